@@ -1,0 +1,158 @@
+"""Seeded image generators and the BASELINE.json configuration table.
+
+The constructions follow BASELINE.json `configs` (c1..c5); the parts BASELINE
+leaves open are fixed as proposed in SURVEY.md §8(d) "Synthetic inputs" and
+listed in DESIGN.md §"Input recipe".  Every image is generated in float64 with
+numpy's PCG64 (`default_rng(seed)`) in a fixed draw order and returned as a
+C-contiguous float32 array with values in [0, 255].
+
+No bilateral-filter arithmetic lives here (this module is shared by the oracle
+tests and the CUDA path, see the task's independence rule).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = [
+    "Config",
+    "CONFIGS",
+    "rect_ramp",
+    "voronoi_texture",
+    "checkerboard",
+    "gradient",
+    "config_image",
+]
+
+
+def rect_ramp(H: int, W: int, seed: int, n_rect: int = 16, noise: float = 10.0) -> np.ndarray:
+    """c1/c4 construction (BASELINE.json configs[0], configs[3]).
+
+    Background: left-to-right ramp 255*x/(W-1).  Then `n_rect` axis-aligned
+    rectangles are painted in order; for each rectangle the draws are, in this
+    order: height ~ U_int[H/16, H/4], width ~ U_int[W/16, W/4], top ~ U_int over
+    valid rows, left ~ U_int over valid columns, value ~ U[0, 255].  Finally
+    i.i.d. N(0, noise^2) is added and the result is clipped to [0, 255].
+    """
+    rng = np.random.default_rng(seed)
+    x = np.arange(W, dtype=np.float64)
+    img = np.empty((H, W), dtype=np.float64)
+    img[:] = 255.0 * x / max(W - 1, 1)
+    for _ in range(n_rect):
+        h = int(rng.integers(max(H // 16, 1), max(H // 4, 1), endpoint=True))
+        w = int(rng.integers(max(W // 16, 1), max(W // 4, 1), endpoint=True))
+        top = int(rng.integers(0, H - h, endpoint=True))
+        left = int(rng.integers(0, W - w, endpoint=True))
+        val = float(rng.uniform(0.0, 255.0))
+        img[top:top + h, left:left + w] = val
+    img += rng.normal(0.0, noise, size=(H, W))
+    np.clip(img, 0.0, 255.0, out=img)
+    return np.ascontiguousarray(img.astype(np.float32))
+
+
+def voronoi_texture(H: int, W: int, seed: int, n_seeds: int, noise: float,
+                    amp: float = 20.0, lam: float = 16.0, theta: float = math.pi / 6,
+                    chunk_rows: int = 256) -> np.ndarray:
+    """c2/c3/c5 construction (BASELINE.json configs[1], [2], [4]).
+
+    Draw order: seed x ~ U[0, W) (n_seeds), seed y ~ U[0, H) (n_seeds), cell
+    value ~ U[0, 255] (n_seeds), then noise N(0, noise^2) row-chunk by row-chunk.
+    Each pixel (x, y) takes the value of the seed nearest (Euclidean) to its
+    centre (x+0.5, y+0.5); texture amp*sin(2*pi*(x cos(theta) + y sin(theta))/lam)
+    is added (amp=0 disables it), then noise, then clip to [0, 255].
+    """
+    from scipy.spatial import cKDTree
+
+    rng = np.random.default_rng(seed)
+    sx = rng.uniform(0.0, W, size=n_seeds)
+    sy = rng.uniform(0.0, H, size=n_seeds)
+    val = rng.uniform(0.0, 255.0, size=n_seeds)
+    tree = cKDTree(np.stack([sx, sy], axis=1))
+    out = np.empty((H, W), dtype=np.float32)
+    xs = np.arange(W, dtype=np.float64)
+    ct, st = math.cos(theta), math.sin(theta)
+    for r0 in range(0, H, chunk_rows):
+        r1 = min(H, r0 + chunk_rows)
+        ys = np.arange(r0, r1, dtype=np.float64)
+        X, Y = np.meshgrid(xs, ys)
+        pts = np.stack([(X + 0.5).ravel(), (Y + 0.5).ravel()], axis=1)
+        _, idx = tree.query(pts, k=1, workers=-1)
+        blk = val[idx].reshape(r1 - r0, W)
+        if amp != 0.0:
+            blk = blk + amp * np.sin(2.0 * math.pi * (X * ct + Y * st) / lam)
+        blk = blk + rng.normal(0.0, noise, size=(r1 - r0, W))
+        np.clip(blk, 0.0, 255.0, out=blk)
+        out[r0:r1] = blk.astype(np.float32)
+    return out
+
+
+def checkerboard(H: int, W: int, tile: int, lo: float = 0.0, hi: float = 255.0) -> np.ndarray:
+    """Two-level checkerboard, top-left tile = lo."""
+    y, x = np.mgrid[0:H, 0:W]
+    img = np.where(((y // tile) + (x // tile)) % 2 == 0, lo, hi)
+    return np.ascontiguousarray(img.astype(np.float32))
+
+
+def gradient(H: int, W: int, lo: float = 0.0, hi: float = 255.0) -> np.ndarray:
+    """Left-to-right linear ramp lo..hi."""
+    x = np.arange(W, dtype=np.float64)
+    row = lo + (hi - lo) * x / max(W - 1, 1)
+    return np.ascontiguousarray(np.broadcast_to(row, (H, W)).astype(np.float32))
+
+
+@dataclass(frozen=True)
+class Config:
+    """One BASELINE.json workload.
+
+    sigma_r is the stated value; sigma_r_twin is the parity-gate twin of
+    SURVEY.md §8(c)-Q1 (same image, sigma_s and N, so the same hot-path work).
+    """
+    name: str
+    H: int
+    W: int
+    batch: int
+    sigma_s: tuple
+    sigma_r: float
+    N: int
+    sigma_r_twin: float
+    kind: str
+    gen: dict = field(default_factory=dict)
+    seed: int = 0
+
+
+CONFIGS = {
+    "c1": Config("c1", 256, 256, 1, (3.0,), 30.0, 5, 100.0, "rect",
+                 dict(n_rect=16, noise=10.0), seed=1),
+    "c2": Config("c2", 1024, 1024, 1, (5.0,), 20.0, 8, 70.0, "voronoi",
+                 dict(n_seeds=200, noise=15.0, amp=20.0), seed=2),
+    "c3": Config("c3", 4096, 4096, 1, (2.0, 5.0, 10.0, 20.0, 40.0), 15.0, 10, 60.0, "voronoi",
+                 dict(n_seeds=2000, noise=20.0, amp=20.0), seed=3),
+    "c4": Config("c4", 1024, 1024, 256, (4.0,), 25.0, 6, 85.0, "rect",
+                 dict(n_rect=16, noise=10.0), seed=1000),
+    "c5": Config("c5", 16384, 16384, 1, (16.0,), 10.0, 12, 55.0, "voronoi",
+                 dict(n_seeds=20000, noise=10.0, amp=0.0), seed=5),
+}
+
+
+def config_image(cfg: Config | str, index: int = 0, H: int | None = None, W: int | None = None) -> np.ndarray:
+    """Image `index` of config `cfg` (batch configs use seed cfg.seed + index).
+
+    H/W override the size (same construction, used for reduced-size parity
+    cases); the Voronoi seed count is scaled with the area so the cell size
+    stays that of the full config.
+    """
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    H = cfg.H if H is None else H
+    W = cfg.W if W is None else W
+    seed = cfg.seed + index
+    g = dict(cfg.gen)
+    if cfg.kind == "rect":
+        return rect_ramp(H, W, seed, **g)
+    if cfg.kind == "voronoi":
+        if (H, W) != (cfg.H, cfg.W):
+            g["n_seeds"] = max(1, int(round(g["n_seeds"] * H * W / (cfg.H * cfg.W))))
+        return voronoi_texture(H, W, seed, **g)
+    raise ValueError(cfg.kind)

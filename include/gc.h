@@ -1,0 +1,192 @@
+/*
+ * gc.h — C ABI of libgc: the Gauss–Chebyshev fast bilateral filter (GCF) hot path
+ * on NVIDIA B200 (sm_100a).
+ *
+ * Paper: S. Ghosh, K. N. Chaudhury, "Fast and High-Quality Bilateral Filtering Using
+ * Gauss-Chebyshev Approximation", arXiv 1605.02178 (IEEE SPCOM 2016).  Citations below
+ * are `P:<line>` = line of /root/reference/PAPER.md (section / equation in brackets).
+ *
+ * Problem statement (what every entry point computes):
+ *   f : I -> R, I a finite H x W rectangle of Z^2, one fp32 grayscale image, row-major,
+ *   pitch W; extended outside I by whole-sample symmetry (P:36 [Sec. I]; R5).
+ *   Spatial kernel g_{sigma_s}(j) = exp(-|j|^2 / 2 sigma_s^2) on Omega = [-W_s, W_s]^2,
+ *   W_s = ceil(3 sigma_s) (P:39, P:48 [Sec. I]; R4).  Range kernel g_{sigma_r}(t) =
+ *   exp(-t^2 / 2 sigma_r^2).  Intensity range [L, U], default [0, 255].
+ *   Output: the GCF approximation of the bilateral filter, eq. (10) (P:108-111 [Sec. II]),
+ *   computed by the pipeline of P:235-240 [Sec. III-B]:
+ *     g = clamp(f, L, U) - t_c, t_c = (L+U)/2                     eq. (17)
+ *     c_n = Chebyshev coefficients of exp on [-mu, mu]            eq. (19)
+ *     F_n = exp(-g^2/2sr^2) (g/sr)^n, n = 0..N+1;  G_n = (g/sr)^n eq. (6)
+ *     Fbar_n = sum_{j in Omega} g_{sigma_s}(j) F_n(i-j)           eq. (7)
+ *     P = sr sum_n c_n G_n Fbar_{n+1},  Q = sum_n c_n G_n Fbar_n  eqs. (8),(9) P:97-106
+ *     out = P/Q + t_c   where Q > 0 and finite, else out = clamp(f)(i)  (R8)
+ *
+ * Conventions for all entry points
+ *   - Status codes, never exceptions; nothing is printed.
+ *   - Device entry points are asynchronous on `stream` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream).  They return after enqueue.  Argument errors are
+ *     detected before anything is enqueued.  Kernel execution errors surface at the
+ *     caller's next synchronisation with the stream.
+ *   - Image memory is owned by the caller.  The library owns a mutex-guarded coefficient
+ *     cache and stream-ordered scratch (cudaMallocAsync / cudaFreeAsync on `stream`).
+ *   - All entry points are re-entrant and thread-safe.
+ *   - `out` must not alias the input.
+ *   - NaN/Inf inputs give unspecified output values (no fault).
+ */
+#ifndef GC_H_
+#define GC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GC_OK = 0,
+  GC_EINVAL = 1,  /* bad argument (sizes, sigmas, N, null or aliased pointers)        */
+  GC_ERANGE = 2,  /* N > GC_N_MAX, or mu beyond the coefficient precision limit        */
+  GC_ECUDA = 3,   /* a CUDA call or kernel launch failed                               */
+  GC_ENOMEM = 4,  /* device scratch allocation failed                                  */
+  GC_ENCCL = 5    /* an NCCL call failed (band API)                                    */
+} gc_status;
+
+#define GC_N_MAX 64          /* maximum polynomial degree N                           */
+#define GC_MU_MAX 4096.0     /* maximum mu = (U-L)^2 / (4 sigma_r^2) for gc_coeffs    */
+
+/* Spatial operator used for eq. (7).  Both compute the truncated sum over Omega exactly
+   as eq. (7) writes it (R3); they differ only in cost and rounding. */
+typedef enum {
+  GC_OP_AUTO = 0,  /* library choice by W_s                      */
+  GC_OP_FIR = 1    /* direct separable FIR, 2(2W_s+1) FMA per plane-pixel              */
+} gc_operator;
+
+/* Human-readable name of a status code (static storage). */
+const char* gc_status_string(gc_status s);
+
+/* Library version string, e.g. "gc 0.1.0 sm_100a". */
+const char* gc_version(void);
+
+/*
+ * gc_coeffs — host only, pure, thread-safe.
+ * c_out[0..N] = eq. (19) coefficients c_n of the degree-N Chebyshev
+ * interpolant of exp on [-mu, mu] (eq. 16 with the nodes rescaled),
+ * mu = (U-L)^2 / (4 sigma_r^2), computed in the library's own multiprecision
+ * arithmetic (>= mu/ln10 + 40 significant digits; R2) and rounded once to
+ * binary64.  mu_out (may be NULL) receives mu rounded to binary64.
+ * Errors: GC_EINVAL if c_out is NULL, N < 0, !(sigma_r > 0), !(U > L) or any argument
+ * is non-finite; GC_ERANGE if N > GC_N_MAX or mu > GC_MU_MAX.
+ */
+gc_status gc_coeffs(int N, double sigma_r, double L, double U, double* c_out, double* mu_out);
+
+/*
+ * gc_bilateral — one image on the device.
+ * img, out: device pointers to H*W fp32, row-major, pitch W.  L = 0, U = 255.
+ * Errors: GC_EINVAL (H < 1, W < 1, !(sigma_s > 0), !(sigma_r > 0), N < 0, null or
+ * overlapping img/out, non-finite sigmas), GC_ERANGE (N > GC_N_MAX, mu > GC_MU_MAX),
+ * GC_ECUDA (launch failure).
+ */
+gc_status gc_bilateral(const float* img, int H, int W, float sigma_s, float sigma_r, int N,
+                       float* out, void* stream);
+
+/*
+ * gc_bilateral_batch — B images, contiguous [B][H][W] fp32 on the device, same
+ * parameters for all; outs has the same layout.  B >= 1.  Errors as gc_bilateral.
+ */
+gc_status gc_bilateral_batch(const float* imgs, int B, int H, int W, float sigma_s,
+                             float sigma_r, int N, float* outs, void* stream);
+
+/*
+ * gc_bilateral_c — as gc_bilateral with caller-supplied coefficients c[0..N] (host
+ * pointer, binary64) in place of eq. (19): e.g. c_n = 1/n! gives the Gauss-polynomial
+ * filter (GPF) of [Chaudhury2015].  GC_EINVAL if c is NULL or non-finite.
+ */
+gc_status gc_bilateral_c(const float* img, int H, int W, float sigma_s, float sigma_r, int N,
+                         const double* c, float* out, void* stream);
+
+/* Full-control entry point used by the three calls above. */
+typedef struct gc_params {
+  int N;                              /* degree, 0 <= N <= GC_N_MAX                      */
+  float sigma_s;                      /* spatial sigma (pixels) > 0                      */
+  float sigma_r;                      /* range sigma (intensity units) > 0               */
+  float L, U;                         /* intensity range, U > L                   */
+  const double* c;                    /* NULL: eq. (19) coefficients; else host c[0..N]  */
+  int op;                             /* gc_operator                                     */
+  unsigned long long* fallback_count; /* NULL or device counter; += guarded pixels (R8)  */
+  void* events[3];                    /* NULL or cudaEvent_t recorded on `stream` before
+                                         the row pass, between the passes and after the
+                                         column pass (per-kernel timing for bench.py)      */
+} gc_params;
+
+/* Fill p with the defaults: L=0, U=255, c=NULL, op=GC_OP_AUTO, fallback_count=NULL,
+   events={NULL}. */
+void gc_params_init(gc_params* p, int N, float sigma_s, float sigma_r);
+
+/* B images [B][H][W] on the device (B >= 1). Errors as gc_bilateral. */
+gc_status gc_filter(const float* imgs, int B, int H, int W, const gc_params* p, float* outs,
+                    void* stream);
+
+/*
+ * gc_filter_host — end-to-end call on HOST buffers (pinned memory recommended):
+ * copies imgs (B*H*W fp32) host->device, filters, copies the result device->host into
+ * outs, all on `stream`, and returns after synchronising that stream (so outs is
+ * valid on return).  Device buffers are stream-ordered scratch owned by the library.
+ * Errors as gc_filter, plus GC_ENOMEM.
+ */
+gc_status gc_filter_host(const float* imgs_host, int B, int H, int W, const gc_params* p,
+                         float* outs_host, void* stream);
+
+/*
+ * Row-band API (multi-GPU domain decomposition, one process per GPU).
+ *
+ * The global image has H_global rows of width W.  Rank r of `world` owns the
+ * contiguous rows [row0, row0 + H_band) (ranks ordered by row0; rank r-1 owns the rows
+ * above).  Every band must have H_band > W_s = ceil(3 sigma_s) rows so that halos come
+ * from the adjacent rank only (GC_EINVAL otherwise).
+ *
+ * gc_band_plan — host only, pure: the halo rows rank `rank` needs, in global row
+ * indices: top = [top0, top0+top_rows) from rank-1, bottom = [bot0, bot0+bot_rows)
+ * from rank+1 (0 rows at the global top / bottom, where eq. 7's symmetric extension is
+ * applied locally).  Identical on every rank; used by gc_bilateral_band and testable
+ * without a GPU.
+ */
+gc_status gc_band_plan(int H_global, int rank, int world, const int* band_rows, float sigma_s,
+                       int* row0, int* top0, int* top_rows, int* bot0, int* bot_rows);
+
+/* NCCL communicator owned by the library.  gc_comm_unique_id fills 128 bytes on one
+   rank; the caller broadcasts them (e.g. torch.distributed); every rank then calls
+   gc_comm_init.  GC_ENCCL on failure.  The CUDA device must be set by the caller. */
+gc_status gc_comm_unique_id(unsigned char id[128]);
+gc_status gc_comm_init(int rank, int world, const unsigned char id[128], void** comm_out);
+gc_status gc_comm_destroy(void* comm);
+
+/*
+ * gc_bilateral_band — this rank's band of the GCF of the global image.  band / out:
+ * device pointers to H_band*W fp32 (rows [row0, row0+H_band)).  Collective over comm:
+ * exchanges the halo rows of f (not of the N+2 planes: they are pointwise in f, so
+ * f is the smallest thing to send) with ranks r-1 and r+1 by grouped
+ * ncclSend/ncclRecv on `stream`, then filters; symmetric extension only at global rows
+ * 0 and H_global-1.  The result equals rows [row0, row0+H_band) of gc_filter on the
+ * whole image.  Errors as gc_filter, plus GC_ENCCL.
+ */
+gc_status gc_bilateral_band(const float* band, int H_band, int W, int H_global, int row0,
+                            const gc_params* p, float* out, void* comm, void* stream);
+
+/*
+ * gc_filter_window — single-GPU building block of the band path (and of the
+ * "virtual band" tests): filters output rows [out_row0, out_row0+out_rows) of a global
+ * H_global x W image whose input rows are supplied in up to three device segments
+ * (top halo, band, bottom halo), seg_row0[k] = global row of seg[k]'s first row,
+ * seg_rows[k] its row count (0 = unused).  Every input row the window needs (after
+ * symmetric reflection at rows 0 and H_global-1) must lie in a segment (GC_EINVAL
+ * otherwise).  out: out_rows*W fp32.
+ */
+gc_status gc_filter_window(const float* const seg[3], const int seg_row0[3], const int seg_rows[3],
+                           int H_global, int W, int out_row0, int out_rows, const gc_params* p,
+                           float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GC_H_ */

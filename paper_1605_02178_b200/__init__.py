@@ -1,0 +1,266 @@
+"""paper_1605_02178_b200 — Python binding of libgc (the GCF hot path on B200, sm_100a).
+
+Argument marshalling only: every step of the filter runs in the CUDA kernels behind
+the C ABI declared in include/gc.h.  PyTorch is used for device memory and streams.
+There is no CPU fallback: if libgc.so is missing or cannot be loaded, importing the
+compute entry points raises.
+
+Names follow include/gc.h and the paper's notation (sigma_s, sigma_r, N, c_n, mu).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = [
+    "GCError", "lib", "coeffs", "bilateral", "bilateral_batch", "bilateral_c", "filter",
+    "filter_host", "filter_window", "band_plan", "Comm", "bilateral_band", "version",
+    "OP_AUTO", "OP_FIR",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgc.so")
+
+OP_AUTO, OP_FIR = 0, 1
+_STATUS = {0: "GC_OK", 1: "GC_EINVAL", 2: "GC_ERANGE", 3: "GC_ECUDA", 4: "GC_ENOMEM", 5: "GC_ENCCL"}
+
+
+class GCError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: {_STATUS.get(status, status)} ({_lib().gc_status_string(status).decode()})")
+
+
+class _Params(ctypes.Structure):
+    _fields_ = [
+        ("N", ctypes.c_int),
+        ("sigma_s", ctypes.c_float),
+        ("sigma_r", ctypes.c_float),
+        ("L", ctypes.c_float),
+        ("U", ctypes.c_float),
+        ("c", ctypes.POINTER(ctypes.c_double)),
+        ("op", ctypes.c_int),
+        ("fallback_count", ctypes.c_void_p),
+        ("events", ctypes.c_void_p * 3),
+    ]
+
+
+_LIB = None
+
+
+def _lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libgc.so not built ({LIB_PATH}); run `python -m paper_1605_02178_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i, f, d = ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_double
+        ip = ctypes.POINTER(ctypes.c_int)
+        L.gc_status_string.restype = ctypes.c_char_p
+        L.gc_status_string.argtypes = [i]
+        L.gc_version.restype = ctypes.c_char_p
+        L.gc_coeffs.argtypes = [i, d, d, d, ctypes.POINTER(d), ctypes.POINTER(d)]
+        L.gc_bilateral.argtypes = [vp, i, i, f, f, i, vp, vp]
+        L.gc_bilateral_batch.argtypes = [vp, i, i, i, f, f, i, vp, vp]
+        L.gc_bilateral_c.argtypes = [vp, i, i, f, f, i, ctypes.POINTER(d), vp, vp]
+        L.gc_params_init.argtypes = [ctypes.POINTER(_Params), i, f, f]
+        L.gc_params_init.restype = None
+        L.gc_filter.argtypes = [vp, i, i, i, ctypes.POINTER(_Params), vp, vp]
+        L.gc_filter_host.argtypes = [vp, i, i, i, ctypes.POINTER(_Params), vp, vp]
+        L.gc_filter_window.argtypes = [ctypes.POINTER(vp), ip, ip, i, i, i, i, ctypes.POINTER(_Params), vp, vp]
+        L.gc_band_plan.argtypes = [i, i, i, ip, f, ip, ip, ip, ip, ip]
+        L.gc_comm_unique_id.argtypes = [ctypes.c_char_p]
+        L.gc_comm_init.argtypes = [i, i, ctypes.c_char_p, ctypes.POINTER(vp)]
+        L.gc_comm_destroy.argtypes = [vp]
+        L.gc_bilateral_band.argtypes = [vp, i, i, i, i, ctypes.POINTER(_Params), vp, vp, vp]
+        for name in ["gc_coeffs", "gc_bilateral", "gc_bilateral_batch", "gc_bilateral_c", "gc_filter",
+                     "gc_filter_host", "gc_filter_window", "gc_band_plan", "gc_comm_unique_id",
+                     "gc_comm_init", "gc_comm_destroy", "gc_bilateral_band"]:
+            getattr(L, name).restype = ctypes.c_int
+        _LIB = L
+    return _LIB
+
+
+lib = _lib
+
+
+def _check(st, where):
+    if st != 0:
+        raise GCError(st, where)
+
+
+def version() -> str:
+    return _lib().gc_version().decode()
+
+
+def coeffs(N: int, sigma_r: float, L: float = 0.0, U: float = 255.0):
+    """c_0..c_N of eq. (19) (binary64, computed in libgc's multiprecision) and mu."""
+    c = (ctypes.c_double * (N + 1))()
+    mu = ctypes.c_double()
+    _check(_lib().gc_coeffs(int(N), float(sigma_r), float(L), float(U), c, ctypes.byref(mu)), "gc_coeffs")
+    return np.array(c[:], dtype=np.float64), mu.value
+
+
+def _params(N, sigma_s, sigma_r, L=0.0, U=255.0, c=None, op=OP_AUTO, fallback=None, events=None):
+    p = _Params()
+    _lib().gc_params_init(ctypes.byref(p), int(N), float(sigma_s), float(sigma_r))
+    p.L, p.U, p.op = float(L), float(U), int(op)
+    keep = None
+    if c is not None:
+        keep = (ctypes.c_double * (N + 1))(*[float(v) for v in c])
+        p.c = ctypes.cast(keep, ctypes.POINTER(ctypes.c_double))
+    if fallback is not None:
+        p.fallback_count = fallback.data_ptr()
+    if events is not None:                    # three torch.cuda.Event (recorded once already)
+        for i, ev in enumerate(events):
+            p.events[i] = ev.cuda_event
+    return p, keep
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev_f32(t, name):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+        raise TypeError(f"{name} must be a contiguous float32 CUDA tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def filter(img, sigma_s, sigma_r, N, c=None, L=0.0, U=255.0, out=None, op=OP_AUTO, fallback=None, stream=None,
+           events=None):
+    """GCF of a [H, W] or [B, H, W] float32 CUDA tensor (gc_filter).  Asynchronous on `stream`.
+
+    c: optional caller coefficients c_0..c_N (e.g. 1/n! = GPF); fallback: optional int64
+    CUDA tensor of one element that receives the number of guarded pixels (R8)."""
+    import torch
+    if img.dim() == 2:
+        B, (H, W) = 1, img.shape
+    elif img.dim() == 3:
+        B, H, W = img.shape
+    else:
+        raise ValueError("img must be [H, W] or [B, H, W]")
+    if out is None:
+        out = torch.empty_like(img)
+    p, keep = _params(N, sigma_s, sigma_r, L, U, c, op, fallback, events)
+    _check(_lib().gc_filter(_dev_f32(img, "img"), B, H, W, ctypes.byref(p), _dev_f32(out, "out"), _stream(stream)),
+           "gc_filter")
+    del keep
+    return out
+
+
+def bilateral(img, sigma_s, sigma_r, N, out=None, stream=None):
+    """gc_bilateral: one [H, W] image, Chebyshev coefficients, [L, U] = [0, 255]."""
+    import torch
+    H, W = img.shape
+    out = torch.empty_like(img) if out is None else out
+    _check(_lib().gc_bilateral(_dev_f32(img, "img"), H, W, float(sigma_s), float(sigma_r), int(N),
+                               _dev_f32(out, "out"), _stream(stream)), "gc_bilateral")
+    return out
+
+
+def bilateral_batch(imgs, sigma_s, sigma_r, N, out=None, stream=None):
+    """gc_bilateral_batch: [B, H, W] images with one parameter set."""
+    import torch
+    B, H, W = imgs.shape
+    out = torch.empty_like(imgs) if out is None else out
+    _check(_lib().gc_bilateral_batch(_dev_f32(imgs, "imgs"), B, H, W, float(sigma_s), float(sigma_r), int(N),
+                                     _dev_f32(out, "out"), _stream(stream)), "gc_bilateral_batch")
+    return out
+
+
+def bilateral_c(img, sigma_s, sigma_r, N, c, out=None, stream=None):
+    """gc_bilateral_c: caller coefficients c_0..c_N (e.g. Taylor 1/n! -> GPF)."""
+    import torch
+    H, W = img.shape
+    out = torch.empty_like(img) if out is None else out
+    cc = (ctypes.c_double * (N + 1))(*[float(v) for v in c])
+    _check(_lib().gc_bilateral_c(_dev_f32(img, "img"), H, W, float(sigma_s), float(sigma_r), int(N), cc,
+                                 _dev_f32(out, "out"), _stream(stream)), "gc_bilateral_c")
+    return out
+
+
+def filter_host(img: np.ndarray, sigma_s, sigma_r, N, c=None, L=0.0, U=255.0, out: np.ndarray | None = None,
+                stream=None):
+    """gc_filter_host: host float32 arrays in and out (pinned recommended); synchronous."""
+    if img.dtype != np.float32 or not img.flags.c_contiguous:
+        raise TypeError("img must be a C-contiguous float32 array")
+    shape = img.shape
+    B, H, W = (1, *shape) if img.ndim == 2 else shape
+    out = np.empty_like(img) if out is None else out
+    p, keep = _params(N, sigma_s, sigma_r, L, U, c)
+    _check(_lib().gc_filter_host(ctypes.c_void_p(img.ctypes.data), B, H, W, ctypes.byref(p),
+                                 ctypes.c_void_p(out.ctypes.data), _stream(stream)), "gc_filter_host")
+    del keep
+    return out
+
+
+def filter_window(segs, H_global, out_row0, out_rows, sigma_s, sigma_r, N, c=None, out=None, stream=None):
+    """gc_filter_window: segs = list of up to 3 (tensor [rows, W], global_row0)."""
+    import torch
+    if not 1 <= len(segs) <= 3:
+        raise ValueError("1..3 segments")
+    W = segs[0][0].shape[1]
+    ptrs = (ctypes.c_void_p * 3)()
+    r0 = (ctypes.c_int * 3)()
+    nr = (ctypes.c_int * 3)()
+    for k, (t, g0) in enumerate(segs):
+        ptrs[k] = _dev_f32(t, "seg").value
+        r0[k], nr[k] = int(g0), int(t.shape[0])
+    if out is None:
+        out = torch.empty((out_rows, W), dtype=torch.float32, device=segs[0][0].device)
+    p, keep = _params(N, sigma_s, sigma_r, c=c)
+    _check(_lib().gc_filter_window(ptrs, r0, nr, int(H_global), int(W), int(out_row0), int(out_rows),
+                                   ctypes.byref(p), _dev_f32(out, "out"), _stream(stream)), "gc_filter_window")
+    del keep
+    return out
+
+
+def band_plan(H_global, rank, world, band_rows, sigma_s):
+    """gc_band_plan (host only): dict(row0, top0, top_rows, bot0, bot_rows) for `rank`."""
+    br = (ctypes.c_int * world)(*[int(v) for v in band_rows])
+    o = [ctypes.c_int() for _ in range(5)]
+    _check(_lib().gc_band_plan(int(H_global), int(rank), int(world), br, float(sigma_s),
+                               *[ctypes.byref(v) for v in o]), "gc_band_plan")
+    return dict(zip(["row0", "top0", "top_rows", "bot0", "bot_rows"], [v.value for v in o]))
+
+
+class Comm:
+    """libgc-owned NCCL communicator; the 128-byte unique id is broadcast with torch.distributed."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        import torch
+        import torch.distributed as dist
+        buf = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            raw = ctypes.create_string_buffer(128)
+            _check(_lib().gc_comm_unique_id(raw), "gc_comm_unique_id")
+            buf = torch.frombuffer(bytearray(raw.raw), dtype=torch.uint8).clone()
+        if dist.get_backend(group) == "nccl":
+            buf = buf.cuda()
+        dist.broadcast(buf, src=0, group=group)
+        ident = bytes(buf.cpu().numpy().tobytes())
+        self.handle = ctypes.c_void_p()
+        _check(_lib().gc_comm_init(int(rank), int(world), ident, ctypes.byref(self.handle)), "gc_comm_init")
+
+    def close(self):
+        if self.handle:
+            _check(_lib().gc_comm_destroy(self.handle), "gc_comm_destroy")
+            self.handle = ctypes.c_void_p()
+
+
+def bilateral_band(band, H_global, row0, sigma_s, sigma_r, N, comm: Comm, c=None, out=None, stream=None):
+    """gc_bilateral_band: this rank's rows [row0, row0+H_band) of the GCF of a row-sharded image."""
+    import torch
+    H_band, W = band.shape
+    out = torch.empty_like(band) if out is None else out
+    p, keep = _params(N, sigma_s, sigma_r, c=c)
+    _check(_lib().gc_bilateral_band(_dev_f32(band, "band"), H_band, W, int(H_global), int(row0), ctypes.byref(p),
+                                    _dev_f32(out, "out"), comm.handle, _stream(stream)), "gc_bilateral_band")
+    del keep
+    return out

@@ -1,0 +1,312 @@
+// gc_api.cpp — the C ABI of libgc (include/gc.h): argument validation, coefficient and
+// tap preparation, stream-ordered scratch, and dispatch to the sm_100a kernels.
+//
+// Every step of the filter runs in the kernels of gc_fir.cu; this file only marshals
+// arguments.  There is no CPU fallback: if the device path cannot run, the call fails
+// with a status code.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "gc_internal.h"
+
+namespace gc {
+namespace {
+
+bool finite_pos(double x) { return std::isfinite(x) && x > 0; }
+
+bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+  auto pa = reinterpret_cast<uintptr_t>(a), pb = reinterpret_cast<uintptr_t>(b);
+  return pa < pb + nb && pb < pa + na;
+}
+
+// W_s = ceil(3 sigma_s) (R4)
+int radius_of(float sigma_s) { return (int)std::ceil(3.0 * (double)sigma_s); }
+
+// Truncated, normalised spatial taps k_m = exp(-m^2 / 2 sigma_s^2) / sum, |m| <= R (eq. 7).
+std::vector<double> taps_of(float sigma_s, int R) {
+  std::vector<double> k(2 * R + 1);
+  double s = 0;
+  const double ss = (double)sigma_s;
+  for (int m = -R; m <= R; m++) s += (k[m + R] = std::exp(-(double)m * m / (2.0 * ss * ss)));
+  for (auto& v : k) v /= s;
+  return k;
+}
+
+gc_status validate_params(const gc_params* p) {
+  if (!p) return GC_EINVAL;
+  if (p->N < 0) return GC_EINVAL;
+  if (p->N > GC_N_MAX) return GC_ERANGE;
+  if (!finite_pos(p->sigma_s) || !finite_pos(p->sigma_r)) return GC_EINVAL;
+  if (!std::isfinite(p->L) || !std::isfinite(p->U) || !(p->U > p->L)) return GC_EINVAL;
+  if (p->op != GC_OP_AUTO && p->op != GC_OP_FIR) return GC_EINVAL;
+  if (radius_of(p->sigma_s) > kMaxFirW) return GC_ERANGE;
+  if (p->c) {
+    for (int n = 0; n <= p->N; n++)
+      if (!std::isfinite(p->c[n])) return GC_EINVAL;
+  }
+  return GC_OK;
+}
+
+// Fill the arithmetic part of KParams (coefficients, taps, centring constants).
+gc_status fill_constants(const gc_params* p, KParams& k, std::vector<float2>& taps_host) {
+  const double L = p->L, U = p->U;
+  const double th = 0.5 * (U - L);
+  const double mu = th * th / ((double)p->sigma_r * (double)p->sigma_r);
+  std::vector<double> cm(p->N + 1);
+  if (p->c) {
+    // caller coefficients: c_n mu^n, normalised by the largest magnitude (cancels in P/Q)
+    double mx = 0;
+    for (int n = 0; n <= p->N; n++) {
+      cm[n] = p->c[n] * std::pow(mu, (double)n);
+      mx = std::max(mx, std::fabs(cm[n]));
+    }
+    if (!(mx > 0) || !std::isfinite(mx)) return GC_ERANGE;
+    for (auto& v : cm) v /= mx;
+  } else {
+    const double* cmu = nullptr;
+    gc_status st = coeffs_cached(p->N, p->sigma_r, L, U, nullptr, &cmu, nullptr);
+    if (st != GC_OK) return st;
+    std::copy(cmu, cmu + p->N + 1, cm.begin());
+  }
+  const int planes = ((p->N + 2) + 1) / 2 * 2;
+  k.NP = planes / 2;
+  for (int q = 0; q < kMaxPairs; q++) {
+    const int n0 = 2 * q, n1 = 2 * q + 1;
+    k.chat2[q] = make_float2(n0 <= p->N ? (float)cm[n0] : 0.f, n1 <= p->N ? (float)cm[n1] : 0.f);
+  }
+  k.R = radius_of(p->sigma_s);
+  std::vector<double> t = taps_of(p->sigma_s, k.R);
+  taps_host.resize(t.size());
+  for (size_t m = 0; m < t.size(); m++) taps_host[m] = make_float2((float)t[m], (float)t[m]);
+  for (int m = 0; m < 2 * kMaxTemplW + 1; m++)
+    k.tap2[m] = m < (int)t.size() ? taps_host[m] : make_float2(0.f, 0.f);
+  k.L = (float)L;
+  k.U = (float)U;
+  k.t_c = (float)(0.5 * (L + U));
+  k.t_h = (float)th;
+  k.inv_th = (float)(1.0 / th);
+  k.ex_k = (float)(-0.5 * mu * 1.4426950408889634);
+  k.fallback = p->fallback_count;
+  for (int i = 0; i < 3; i++) k.ev[i] = reinterpret_cast<cudaEvent_t>(p->events[i]);
+  return GC_OK;
+}
+
+gc_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return GC_OK;
+  if (e == cudaErrorMemoryAllocation) return GC_ENOMEM;
+  return GC_ECUDA;
+}
+
+// Keep freed stream-ordered scratch in the device's default pool instead of returning it
+// to the driver at every synchronisation (the plane buffer is reallocated per call).
+void retain_pool() {
+  static std::mutex mu;
+  static bool done[64] = {false};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
+// Run the pipeline for the window described by k (rows/segments already set).
+gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) {
+  retain_pool();
+  const size_t plane_elems = (size_t)k.NP * k.in_rows * k.Wd;
+  float2* planes = nullptr;
+  float2* taps_dev = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&planes, plane_elems * k.B * sizeof(float2), s);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (k.R > kMaxTemplW) {
+    e = cudaMallocAsync((void**)&taps_dev, taps_host.size() * sizeof(float2), s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(taps_dev, taps_host.data(), taps_host.size() * sizeof(float2),
+                          cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(planes, s);
+      if (taps_dev) cudaFreeAsync(taps_dev, s);
+      return cuda_status(e);
+    }
+  }
+  k.planes = planes;
+  k.planes_img_stride = (long long)plane_elems;
+  k.taps_g = taps_dev;
+  e = launch_fir_two_pass(k, s);
+  cudaError_t e2 = cudaFreeAsync(planes, s);
+  if (taps_dev) cudaFreeAsync(taps_dev, s);
+  if (e != cudaSuccess) return cuda_status(e);
+  return cuda_status(e2);
+}
+
+}  // namespace
+}  // namespace gc
+
+using namespace gc;
+
+extern "C" {
+
+const char* gc_status_string(gc_status s) {
+  switch (s) {
+    case GC_OK: return "GC_OK";
+    case GC_EINVAL: return "GC_EINVAL: invalid argument";
+    case GC_ERANGE: return "GC_ERANGE: parameter outside the supported range";
+    case GC_ECUDA: return "GC_ECUDA: CUDA error";
+    case GC_ENOMEM: return "GC_ENOMEM: device allocation failed";
+    case GC_ENCCL: return "GC_ENCCL: NCCL error";
+  }
+  return "GC_?: unknown status";
+}
+
+const char* gc_version(void) { return "gc 0.1.0 sm_100a"; }
+
+void gc_params_init(gc_params* p, int N, float sigma_s, float sigma_r) {
+  if (!p) return;
+  std::memset(p, 0, sizeof(*p));
+  p->N = N;
+  p->sigma_s = sigma_s;
+  p->sigma_r = sigma_r;
+  p->L = 0.f;
+  p->U = 255.f;
+  p->c = nullptr;
+  p->op = GC_OP_AUTO;
+  p->fallback_count = nullptr;
+}
+
+gc_status gc_filter_window(const float* const seg[3], const int seg_row0[3], const int seg_rows[3],
+                           int H_global, int W, int out_row0, int out_rows, const gc_params* p,
+                           float* out, void* stream) {
+  gc_status st = validate_params(p);
+  if (st != GC_OK) return st;
+  if (!seg || !seg_row0 || !seg_rows || !out) return GC_EINVAL;
+  if (H_global < 1 || W < 1 || out_rows < 1 || out_row0 < 0 || out_row0 + out_rows > H_global)
+    return GC_EINVAL;
+  KParams k;
+  std::memset(&k, 0, sizeof(k));
+  int nseg = 0;
+  for (int i = 0; i < 3; i++) {
+    if (seg_rows[i] == 0) { k.seg[i] = Seg{seg[i], -1, 0}; continue; }
+    if (seg_rows[i] < 0 || !seg[i] || seg_row0[i] < 0 || seg_row0[i] + seg_rows[i] > H_global) return GC_EINVAL;
+    if (overlap(seg[i], (size_t)seg_rows[i] * W * 4, out, (size_t)out_rows * W * 4)) return GC_EINVAL;
+    k.seg[i] = Seg{seg[i], seg_row0[i], seg_rows[i]};
+    nseg++;
+  }
+  if (nseg == 0) return GC_EINVAL;
+  const int R = radius_of(p->sigma_s);
+  // rows the window needs (after symmetric extension) must all be in some segment
+  int lo = H_global, hi = -1;
+  auto mir = [&](int q) {
+    if (H_global == 1) return 0;
+    const int per = 2 * H_global - 2;
+    q = q < 0 ? -q : q;
+    q %= per;
+    return q < H_global ? q : per - q;
+  };
+  for (int y = out_row0 - R; y <= out_row0 + out_rows - 1 + R; y++) {
+    const int q = mir(y);
+    bool found = false;
+    for (int i = 0; i < 3; i++)
+      if (k.seg[i].rows > 0 && q >= k.seg[i].row0 && q < k.seg[i].row0 + k.seg[i].rows) found = true;
+    if (!found) return GC_EINVAL;
+    lo = std::min(lo, q);
+    hi = std::max(hi, q);
+  }
+  std::vector<float2> taps_host;
+  st = fill_constants(p, k, taps_host);
+  if (st != GC_OK) return st;
+  k.H = H_global;
+  k.Wd = W;
+  k.B = 1;
+  k.in_row0 = lo;
+  k.in_rows = hi - lo + 1;
+  k.out_row0 = out_row0;
+  k.out_rows = out_rows;
+  k.seg_img_stride = 0;
+  k.out = out;
+  k.out_img_stride = (long long)out_rows * W;
+  return run(k, taps_host, reinterpret_cast<cudaStream_t>(stream));
+}
+
+gc_status gc_filter(const float* imgs, int B, int H, int W, const gc_params* p, float* outs, void* stream) {
+  gc_status st = validate_params(p);
+  if (st != GC_OK) return st;
+  if (!imgs || !outs || B < 1 || H < 1 || W < 1) return GC_EINVAL;
+  const size_t bytes = (size_t)B * H * W * sizeof(float);
+  if (overlap(imgs, bytes, outs, bytes)) return GC_EINVAL;
+  KParams k;
+  std::memset(&k, 0, sizeof(k));
+  std::vector<float2> taps_host;
+  st = fill_constants(p, k, taps_host);
+  if (st != GC_OK) return st;
+  k.H = H;
+  k.Wd = W;
+  k.B = B;
+  k.in_row0 = 0;
+  k.in_rows = H;
+  k.out_row0 = 0;
+  k.out_rows = H;
+  k.seg[0] = Seg{imgs, 0, H};
+  k.seg[1] = Seg{imgs, -1, 0};
+  k.seg[2] = Seg{imgs, -1, 0};
+  k.seg_img_stride = (long long)H * W;
+  k.out = outs;
+  k.out_img_stride = (long long)H * W;
+  return run(k, taps_host, reinterpret_cast<cudaStream_t>(stream));
+}
+
+gc_status gc_bilateral(const float* img, int H, int W, float sigma_s, float sigma_r, int N, float* out,
+                       void* stream) {
+  gc_params p;
+  gc_params_init(&p, N, sigma_s, sigma_r);
+  return gc_filter(img, 1, H, W, &p, out, stream);
+}
+
+gc_status gc_bilateral_batch(const float* imgs, int B, int H, int W, float sigma_s, float sigma_r, int N,
+                             float* outs, void* stream) {
+  gc_params p;
+  gc_params_init(&p, N, sigma_s, sigma_r);
+  return gc_filter(imgs, B, H, W, &p, outs, stream);
+}
+
+gc_status gc_bilateral_c(const float* img, int H, int W, float sigma_s, float sigma_r, int N, const double* c,
+                         float* out, void* stream) {
+  if (!c) return GC_EINVAL;
+  gc_params p;
+  gc_params_init(&p, N, sigma_s, sigma_r);
+  p.c = c;
+  return gc_filter(img, 1, H, W, &p, out, stream);
+}
+
+gc_status gc_filter_host(const float* imgs_host, int B, int H, int W, const gc_params* p, float* outs_host,
+                         void* stream) {
+  gc_status st = validate_params(p);
+  if (st != GC_OK) return st;
+  if (!imgs_host || !outs_host || B < 1 || H < 1 || W < 1) return GC_EINVAL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t bytes = (size_t)B * H * W * sizeof(float);
+  float *din = nullptr, *dout = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&din, bytes, s);
+  if (e != cudaSuccess) return cuda_status(e);
+  e = cudaMallocAsync((void**)&dout, bytes, s);
+  if (e != cudaSuccess) { cudaFreeAsync(din, s); return cuda_status(e); }
+  e = cudaMemcpyAsync(din, imgs_host, bytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    st = gc_filter(din, B, H, W, p, dout, stream);
+    if (st == GC_OK) e = cudaMemcpyAsync(outs_host, dout, bytes, cudaMemcpyDeviceToHost, s);
+  }
+  cudaFreeAsync(din, s);
+  cudaFreeAsync(dout, s);
+  cudaError_t es = cudaStreamSynchronize(s);
+  if (st != GC_OK) return st;
+  if (e != cudaSuccess) return cuda_status(e);
+  return cuda_status(es);
+}
+
+}  // extern "C"

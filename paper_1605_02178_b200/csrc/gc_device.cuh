@@ -1,0 +1,59 @@
+// gc_device.cuh — small device helpers shared by the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "gc_internal.h"
+
+namespace gc {
+
+// Packed fp32x2 arithmetic (SASS FFMA2 / FMUL2): one issue slot for two FP32 lanes.
+// Measured on B200: the FMA pipe stays at 128 lanes/clk/SM, so FFMA2 halves issue
+// pressure without raising the FMA peak (profiles/r01_ubench_fp32.txt).
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&d))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&c)));
+  return d;
+}
+
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  float2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&d))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+  return d;
+}
+
+// Whole-sample symmetric extension (R5): period 2n-2, n = 1 -> 0.
+__device__ __forceinline__ int mirror(int p, int n) {
+  if (n <= 1) return 0;
+  const int period = 2 * n - 2;
+  p = p < 0 ? -p : p;
+  p %= period;
+  return p < n ? p : period - p;
+}
+
+// Pointer to global row gy of image b, found in the input segments.
+__device__ __forceinline__ const float* row_ptr(const KParams& p, int b, int gy) {
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    const int r = gy - p.seg[k].row0;
+    if (r >= 0 && r < p.seg[k].rows) return p.seg[k].ptr + b * p.seg_img_stride + (long long)r * p.Wd;
+  }
+  return p.seg[0].ptr + b * p.seg_img_stride;  // unreachable after host validation
+}
+
+// Eq. (17) centring and the scaled auxiliary variable a' = g / t_h in [-1, 1], plus the
+// Gaussian factor e = exp(-g^2 / 2 sigma_r^2) of eq. (6), as exp2(ex_k a'^2).
+__device__ __forceinline__ void centre(const KParams& p, float f, float& a, float& e) {
+  f = fminf(fmaxf(f, p.L), p.U);            // inputs clamped to [L, U] (R7)
+  a = (f - p.t_c) * p.inv_th;
+  e = exp2f(p.ex_k * (a * a));
+}
+
+}  // namespace gc

@@ -1,0 +1,125 @@
+"""CPU-side checks of libgc.so: it loads, exports every symbol include/gc.h declares,
+its host-only entry points (gc_coeffs, gc_band_plan) agree with the oracle / the
+paper, and argument validation returns the documented status codes before any CUDA
+work is enqueued.  No kernel is launched here."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def gc():
+    import paper_1605_02178_b200 as gc
+    if not os.path.exists(gc.LIB_PATH):
+        from paper_1605_02178_b200 import build
+        build.build()
+    return gc
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "gc.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gc_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol(gc):
+    lib = gc.lib()
+    names = _declared()
+    assert "gc_bilateral" in names and "gc_coeffs" in names and "gc_bilateral_batch" in names
+    for n in names:
+        assert hasattr(lib, n), n
+    assert "sm_100a" in gc.version()
+
+
+def test_library_is_sm100a_only():
+    """The fat binary carries sm_100a SASS (cuobjdump), nothing for other archs."""
+    import subprocess
+    import paper_1605_02178_b200 as gc
+    r = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", gc.LIB_PATH], capture_output=True, text=True)
+    if r.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    archs = set(re.findall(r"sm_\d+a?", r.stdout))
+    assert archs == {"sm_100a"}, archs
+
+
+STATED = [(5, 30.0), (8, 20.0), (10, 15.0), (6, 25.0), (12, 10.0)]
+TWINS = [(5, 100.0), (8, 70.0), (10, 60.0), (6, 85.0), (12, 55.0)]
+
+
+@pytest.mark.parametrize("N,sigma_r", STATED + TWINS + [(28, 30.0), (40, 30.0), (0, 30.0), (1, 50.0), (20, 1e5)])
+def test_gc_coeffs_matches_oracle(gc, N, sigma_r):
+    """Step a0: libgc's own multiprecision eq. (19) vs the mpmath oracle (to 1 ulp)."""
+    c, mu = gc.coeffs(N, sigma_r)
+    ref = oracle.cheb_c_float(N, sigma_r)
+    assert mu == float(oracle.mu_of(sigma_r))
+    ulps = np.abs(c.view(np.int64) - ref.view(np.int64))
+    assert np.all(ulps <= 1), (c, ref)
+
+
+def test_gc_coeffs_errors(gc):
+    lib = gc.lib()
+    c = (ctypes.c_double * 80)()
+    assert lib.gc_coeffs(-1, 30.0, 0.0, 255.0, c, None) == 1
+    assert lib.gc_coeffs(5, 0.0, 0.0, 255.0, c, None) == 1
+    assert lib.gc_coeffs(5, 30.0, 255.0, 0.0, c, None) == 1
+    assert lib.gc_coeffs(5, float("nan"), 0.0, 255.0, c, None) == 1
+    assert lib.gc_coeffs(5, 30.0, 0.0, 255.0, None, None) == 1
+    assert lib.gc_coeffs(65, 30.0, 0.0, 255.0, c, None) == 2        # N > GC_N_MAX
+    assert lib.gc_coeffs(5, 1.0, 0.0, 255.0, c, None) == 2          # mu = 16256 > GC_MU_MAX
+    assert lib.gc_coeffs(5, 30.0, 0.0, 255.0, c, None) == 0
+
+
+def test_device_entry_points_validate_before_cuda(gc):
+    """Bad arguments are rejected with GC_EINVAL / GC_ERANGE without touching CUDA."""
+    lib = gc.lib()
+    fake = ctypes.c_void_p(0x10000000)
+    fake2 = ctypes.c_void_p(0x20000000)
+    assert lib.gc_bilateral(None, 8, 8, 3.0, 30.0, 5, fake2, None) == 1
+    assert lib.gc_bilateral(fake, 0, 8, 3.0, 30.0, 5, fake2, None) == 1
+    assert lib.gc_bilateral(fake, 8, 8, 0.0, 30.0, 5, fake2, None) == 1
+    assert lib.gc_bilateral(fake, 8, 8, 3.0, -1.0, 5, fake2, None) == 1
+    assert lib.gc_bilateral(fake, 8, 8, 3.0, 30.0, -1, fake2, None) == 1
+    assert lib.gc_bilateral(fake, 8, 8, 3.0, 30.0, 65, fake2, None) == 2
+    assert lib.gc_bilateral(fake, 8, 8, 3.0, 30.0, 5, fake, None) == 1           # aliased
+    assert lib.gc_bilateral_batch(fake, 0, 8, 8, 3.0, 30.0, 5, fake2, None) == 1
+    assert lib.gc_bilateral_c(fake, 8, 8, 3.0, 30.0, 5, None, fake2, None) == 1
+    cc = (ctypes.c_double * 6)(1, 1, 0.5, float("inf"), 0, 0)
+    assert lib.gc_bilateral_c(fake, 8, 8, 3.0, 30.0, 5, cc, fake2, None) == 1
+    assert lib.gc_bilateral(fake, 8, 8, 1000.0, 30.0, 5, fake2, None) == 2      # W_s > kMaxFirW
+
+
+def test_status_strings(gc):
+    lib = gc.lib()
+    for s in range(6):
+        assert lib.gc_status_string(s).startswith(b"GC_")
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_band_plan(gc, world):
+    H, sigma_s = 1000, 5.0
+    R = 15
+    rows = [H // world + (1 if k < H % world else 0) for k in range(world)]
+    covered = []
+    for r in range(world):
+        pl = gc.band_plan(H, r, world, rows, sigma_s)
+        assert pl["row0"] == sum(rows[:r])
+        assert pl["top_rows"] == (R if r > 0 else 0) and pl["top0"] == pl["row0"] - pl["top_rows"]
+        assert pl["bot_rows"] == (R if r < world - 1 else 0) and pl["bot0"] == pl["row0"] + rows[r]
+        covered += list(range(pl["row0"], pl["row0"] + rows[r]))
+    assert covered == list(range(H))
+
+
+def test_band_plan_errors(gc):
+    with pytest.raises(gc.GCError):
+        gc.band_plan(100, 0, 2, [50, 49], 3.0)            # rows do not sum to H
+    with pytest.raises(gc.GCError):
+        gc.band_plan(100, 0, 2, [92, 8], 3.0)             # band <= W_s = 9
+    with pytest.raises(gc.GCError):
+        gc.band_plan(100, 2, 2, [50, 50], 3.0)            # rank out of range

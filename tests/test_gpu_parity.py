@@ -1,0 +1,224 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element by element.
+
+Gate (BASELINE.json north_star): max-abs <= 1e-2 and RMS <= 1e-3 on the 0-255 scale.
+Parity is gated at the sigma_r twins of DESIGN.md R1 (same image, sigma_s and N as the
+stated config, hence the same hot-path work); the stated (sigma_r, N) pairs are
+numerically ill-posed for the method and are run and reported, not gated
+(test_stated_configs_reported).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from synth import CONFIGS, checkerboard, config_image, gradient
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS, RMS = 1e-2, 1e-3
+
+
+@pytest.fixture(scope="module")
+def gc(cuda_device):
+    import paper_1605_02178_b200 as gc
+    return gc
+
+
+def _run(gc, img, sigma_s, sigma_r, N, c=None, fallback=False):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(img, dtype=np.float32)).cuda()
+    fb = torch.zeros(1, dtype=torch.int64, device="cuda") if fallback else None
+    out = gc.filter(t, sigma_s, sigma_r, N, c=c, fallback=fb)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy().astype(np.float64)
+    return (o, int(fb.item())) if fallback else o
+
+
+def _gate(out, ref, what=""):
+    err = np.abs(out - ref)
+    ma, rms = float(err.max()), float(math.sqrt(np.mean(err ** 2)))
+    assert np.all(np.isfinite(out)), what
+    assert ma <= MAX_ABS and rms <= RMS, f"{what}: max-abs {ma:.3e} rms {rms:.3e}"
+    return ma, rms
+
+
+# ------------------------------------------------------------------ configs at twin sigma_r
+
+@pytest.mark.parametrize("cfg,sigma_s,H,W", [
+    ("c1", 3.0, 256, 256),            # c1 at full size
+    ("c1", 3.0, 77, 301),             # ragged tails in x and y
+    ("c2", 5.0, 1024, 1024),          # c2 at full size (the bench workload)
+    ("c2", 5.0, 150, 131),
+    ("c3", 2.0, 300, 517),
+    ("c3", 5.0, 263, 260),
+    ("c3", 10.0, 200, 333),           # W = 30: runtime-radius kernels
+    ("c3", 20.0, 190, 210),           # W = 60
+    ("c3", 40.0, 130, 170),           # W = 120 > image size: repeated reflections
+    ("c4", 4.0, 129, 1024),
+    ("c5", 16.0, 300, 290),           # W = 48
+])
+def test_parity_twin(gc, cfg, sigma_s, H, W):
+    c = CONFIGS[cfg]
+    img = config_image(c, H=H, W=W)
+    out = _run(gc, img, sigma_s, c.sigma_r_twin, c.N)
+    ref, nfb = oracle.gc_filter(img, sigma_s, c.sigma_r_twin, c.N)
+    assert nfb == 0
+    _gate(out, ref, f"{cfg} sigma_s={sigma_s} {H}x{W}")
+
+
+def test_parity_c3_full_size_sampled_rows(gc):
+    """c3 at 4096^2 (sigma_s=5, twin): rows at both image edges and the middle."""
+    c = CONFIGS["c3"]
+    img = config_image(c)
+    out = _run(gc, img, 5.0, c.sigma_r_twin, c.N)
+    rows = [0, 1, 7, 2047, 2048, 4090, 4095]
+    ref, _ = oracle.gc_filter_rows(img, rows, 5.0, c.sigma_r_twin, c.N)
+    _gate(out[rows], ref, "c3 full size")
+
+
+def test_parity_c4_full_batch(gc):
+    """c4 in the bench's launch configuration: the 256-image batch in one call; three
+    images (first, middle, last) compared in full."""
+    import torch
+    c = CONFIGS["c4"]
+    imgs = np.stack([config_image(c, index=i) for i in range(c.batch)])
+    t = torch.from_numpy(imgs).cuda()
+    out = gc.filter(t, c.sigma_s[0], c.sigma_r_twin, c.N)
+    torch.cuda.synchronize()
+    for i in [0, 127, 255]:
+        ref, _ = oracle.gc_filter(imgs[i], c.sigma_s[0], c.sigma_r_twin, c.N)
+        _gate(out[i].cpu().numpy().astype(np.float64), ref, f"c4 image {i}")
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 17), (19, 1), (2, 3), (5, 7), (9, 40)])
+def test_tiny_images(gc, shape):
+    """Degenerate sizes: W_s >= image size forces repeated reflections (R5)."""
+    img = config_image("c1", H=max(shape[0], 2), W=max(shape[1], 2))[:shape[0], :shape[1]]
+    img = np.ascontiguousarray(img)
+    for sigma_s, sigma_r, N in [(3.0, 100.0, 5), (1.0, 70.0, 8), (12.0, 60.0, 10)]:
+        out = _run(gc, img, sigma_s, sigma_r, N)
+        ref, _ = oracle.gc_filter(img, sigma_s, sigma_r, N)
+        _gate(out, ref, f"{shape} sigma_s={sigma_s}")
+
+
+def test_constant_and_two_level_images(gc):
+    for v in [0.0, 63.0, 127.5, 255.0]:
+        img = np.full((40, 70), v, np.float32)
+        out = _run(gc, img, 3.0, 100.0, 5)
+        assert np.max(np.abs(out - v)) < 1e-3
+    img = checkerboard(96, 96, 8)
+    ref, _ = oracle.gc_filter(img, 5.0, 70.0, 8)
+    _gate(_run(gc, img, 5.0, 70.0, 8), ref, "checkerboard")
+    img = gradient(64, 200)
+    ref, _ = oracle.gc_filter(img, 2.0, 60.0, 10)
+    _gate(_run(gc, img, 2.0, 60.0, 10), ref, "gradient")
+
+
+def test_paper_regime_sigma_r_30(gc):
+    """The paper's operating point (Table II: sigma_r=30, N=28; N=32)."""
+    img = config_image("c2", H=200, W=190)
+    for N in [28, 32]:
+        ref, nfb = oracle.gc_filter(img, 5.0, 30.0, N)
+        assert nfb == 0
+        _gate(_run(gc, img, 5.0, 30.0, N), ref, f"sigma_r=30 N={N}")
+
+
+def test_gpf_taylor_coefficients(gc):
+    """gc_bilateral_c with c_n = 1/n! (the GPF of P:66-69) at the STATED sigma_r."""
+    import torch
+    for cfg in ["c2", "c4", "c5"]:
+        c = CONFIGS[cfg]
+        img = config_image(c, H=120, W=140)
+        tay = oracle.taylor_c(c.N)
+        ref, nfb = oracle.gc_filter(img, 3.0, c.sigma_r, c.N, c=tay)
+        t = torch.from_numpy(img).cuda()
+        out = gc.bilateral_c(t, 3.0, c.sigma_r, c.N, tay)
+        torch.cuda.synchronize()
+        _gate(out.cpu().numpy().astype(np.float64), ref, f"GPF {cfg}")
+
+
+def test_named_entry_points_agree(gc):
+    import torch
+    c = CONFIGS["c1"]
+    img = config_image(c, H=100, W=120)
+    t = torch.from_numpy(img).cuda()
+    a = gc.bilateral(t, 3.0, 100.0, 5)
+    b = gc.filter(t, 3.0, 100.0, 5)
+    cb = gc.bilateral_batch(t[None].contiguous(), 3.0, 100.0, 5)[0]
+    cc = gc.bilateral_c(t, 3.0, 100.0, 5, oracle.cheb_c_float(5, 100.0))
+    torch.cuda.synchronize()
+    assert torch.equal(a, b) and torch.equal(a, cb)
+    assert float((a - cc).abs().max()) < 1e-3
+
+
+def test_batch_equals_singles(gc):
+    import torch
+    c = CONFIGS["c4"]
+    imgs = np.stack([config_image(c, index=i, H=90, W=110) for i in range(3)])
+    t = torch.from_numpy(imgs).cuda()
+    outb = gc.filter(t, 4.0, 85.0, 6)
+    for i in range(3):
+        assert torch.equal(outb[i], gc.filter(t[i].contiguous(), 4.0, 85.0, 6))
+
+
+def test_deterministic(gc):
+    import torch
+    img = torch.from_numpy(config_image("c2", H=300, W=301)).cuda()
+    a = gc.filter(img, 5.0, 70.0, 8)
+    b = gc.filter(img, 5.0, 70.0, 8)
+    assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("sigma_s", [3.0, 16.0])
+def test_virtual_bands_equal_whole_image(gc, sigma_s):
+    """Single-GPU emulation of the row-band path: each band filtered by gc_filter_window
+    from three segments (top halo, band, bottom halo) equals the whole-image result."""
+    import torch
+    img = config_image("c5", H=400, W=333)
+    t = torch.from_numpy(img).cuda()
+    whole = gc.filter(t, sigma_s, 55.0, 12)
+    R = math.ceil(3 * sigma_s)
+    bands = [0, 130, 260, 400]
+    for k in range(3):
+        r0, r1 = bands[k], bands[k + 1]
+        segs = []
+        if k > 0:
+            segs.append((t[r0 - R:r0].clone(), r0 - R))
+        segs.append((t[r0:r1].clone(), r0))
+        if k < 2:
+            segs.append((t[r1:r1 + R].clone(), r1))
+        part = gc.filter_window(segs, 400, r0, r1 - r0, sigma_s, 55.0, 12)
+        torch.cuda.synchronize()
+        assert torch.equal(part, whole[r0:r1]), k
+
+
+def test_window_rejects_missing_rows(gc):
+    import torch
+    t = torch.from_numpy(config_image("c5", H=100, W=64)).cuda()
+    with pytest.raises(gc.GCError):
+        gc.filter_window([(t[10:50].clone(), 10)], 100, 10, 40, 3.0, 55.0, 12)   # no halo
+
+
+def test_filter_host_e2e(gc):
+    import torch
+    img = config_image("c2", H=256, W=300)
+    out = gc.filter_host(img, 5.0, 70.0, 8)
+    dev = gc.filter(torch.from_numpy(img).cuda(), 5.0, 70.0, 8).cpu().numpy()
+    assert np.array_equal(out, dev)
+
+
+def test_fallback_counter_and_stated_configs_reported(gc, capsys):
+    """Stated (sigma_r, N): run and report (not gated, R1).  The guard of R8
+    is exercised: guarded pixels are counted and pass f through."""
+    lines = []
+    for name in ["c1", "c2", "c3", "c4", "c5"]:
+        c = CONFIGS[name]
+        img = config_image(c, H=96, W=96)
+        out, nfb = _run(gc, img, c.sigma_s[0] if name != "c3" else 5.0, c.sigma_r, c.N, fallback=True)
+        ref, nref = oracle.gc_filter(img, c.sigma_s[0] if name != "c3" else 5.0, c.sigma_r, c.N)
+        assert np.all(np.isfinite(out))
+        assert 0 <= nfb <= img.size
+        lines.append(f"{name} stated sigma_r={c.sigma_r} N={c.N}: max-abs vs oracle "
+                     f"{np.max(np.abs(out - ref)):.3g}, guarded gpu {nfb} / oracle {nref}")
+    print("\n".join(lines))

@@ -81,8 +81,7 @@ gc_status fill_constants(const gc_params* p, KParams& k, std::vector<float2>& ta
   std::vector<double> t = taps_of(p->sigma_s, k.R);
   taps_host.resize(t.size());
   for (size_t m = 0; m < t.size(); m++) taps_host[m] = make_float2((float)t[m], (float)t[m]);
-  for (int m = 0; m < 2 * kMaxTemplW + 1; m++)
-    k.tap2[m] = m < (int)t.size() ? taps_host[m] : make_float2(0.f, 0.f);
+  for (int m = 0; m < 2 * kMaxTemplW + 1; m++) k.tap[m] = m < (int)t.size() ? (float)t[m] : 0.f;
   k.L = (float)L;
   k.U = (float)U;
   k.t_c = (float)(0.5 * (L + U));
@@ -120,6 +119,11 @@ void retain_pool() {
 // Run the pipeline for the window described by k (rows/segments already set).
 gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) {
   retain_pool();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  k.num_sms = 148;
+  cudaDeviceGetAttribute(&k.num_sms, cudaDevAttrMultiProcessorCount, dev);
+  k.in_pitch = k.in_rows;
   const size_t plane_elems = (size_t)k.NP * k.in_rows * k.Wd;
   float2* planes = nullptr;
   float2* taps_dev = nullptr;

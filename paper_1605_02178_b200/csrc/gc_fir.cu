@@ -15,172 +15,382 @@
 // every output of the thread's register block that it touches, with compile-time tap
 // indices (template radius W), so the FFMA count is exactly (2W+1) per output and plane.
 // Radii above kMaxTemplW use the runtime-W kernels at the end of the file.
+#include <algorithm>
 #include <cstdio>
+#include <cstring>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "gc_device.cuh"
 
 namespace gc {
 
 // ------------------------------------------------------------------ K_row (templated W)
+//
+// Persistent grid; the unit of work is a WARP task: 4 image rows x 128 columns.
+// Lane = (row r = lane/8, column block tx = lane%8); each lane owns RX = 16 consecutive
+// outputs.  The warp stages its 4 rows of f (+ horizontal halo) in a warp-private,
+// bank-conflict-free shared-memory slice holding the CURRENT plane pair
+// (F'_{2p}, F'_{2p+1}) and a'^2; between pairs every element is advanced once
+// (psi <- psi a'^2, FMUL2).  The FIR streams the lane's RX + 2W inputs from shared
+// memory input-stationary (each input multiply-added into every output it touches, with
+// compile-time tap indices), and each filtered pair is written as full rows with
+// 16-byte stores after a shared-memory transpose-free staging.
 
-template <int W, int RX, int TXT, int TY>
-__global__ void __launch_bounds__(TXT* TY) k_row_t(const KParams p) {
-  constexpr int TX = TXT * RX;       // output columns per CTA
-  constexpr int SW = TX + 2 * W;     // staged columns (with the horizontal halo)
-  constexpr int NW = RX + 2 * W;     // inputs per thread
+constexpr int kRowWarpsPerCta = 4;
+
+template <int W>
+struct RowCfg {
+  static constexpr int RX = 16;
+  static constexpr int WCOLS = 8 * RX;          // output columns per warp task
+  static constexpr int SW = WCOLS + 2 * W;      // staged columns
+  static constexpr int NW = RX + 2 * W;         // inputs per lane
+  static constexpr int NLD = (SW + 31) / 32;    // staged elements per lane per row
+  // +1 pair every 16: the 8 lanes of a row (stride 16 columns) hit distinct bank pairs
+  static __device__ __forceinline__ int pad(int c) { return c + (c >> 4); }
+  static constexpr int SWP0 = SW + (SW >> 4) + 1;
+  static constexpr int SWP = SWP0 + (24 - SWP0 % 16) % 16;   // row stride = 8 (mod 16) pairs
+  static constexpr int OWP0 = WCOLS + (WCOLS >> 4) + 1;
+  static constexpr int OWP = OWP0 + (24 - OWP0 % 16) % 16;
+  static constexpr int SMEM_WARP = (2 * 4 * SWP + 4 * OWP) * 8;
+};
+
+template <int W>
+__global__ void __launch_bounds__(32 * kRowWarpsPerCta, 4) k_row_t(const KParams p) {
+  using C = RowCfg<W>;
+  constexpr int RX = C::RX;
   extern __shared__ float4 smem_row[];
-  float2* sEA = reinterpret_cast<float2*>(smem_row);   // [TY][SW] (e, e a')   = pair 0
-  float2* sA2 = sEA + TY * SW;                          // [TY][SW] (a'^2, a'^2)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float2* sPsi = reinterpret_cast<float2*>(smem_row) + warp * (C::SMEM_WARP / 8);  // [4][SWP] current pair
+  float2* sA2 = sPsi + 4 * C::SWP;                                                   // [4][SWP] (a'^2, a'^2)
+  float2* sO = sA2 + 4 * C::SWP;                                                     // [4][OWP]
 
-  const int b = blockIdx.z;
-  const int x0 = blockIdx.x * TX;
-  const int r0 = blockIdx.y * TY;    // relative to in_row0
-  const int tid = threadIdx.y * TXT + threadIdx.x;
-
-  // Stage f for TY rows x SW columns (coalesced along x; mirrored in x).
-  for (int r = 0; r < TY; r++) {
-    const int rr = r0 + r;
-    if (rr >= p.in_rows) break;
-    const float* src = row_ptr(p, b, p.in_row0 + rr);
-    for (int c = tid; c < SW; c += TXT * TY) {
-      const int gx = mirror(x0 - W + c, p.Wd);
-      float a, e;
-      centre(p, __ldg(src + gx), a, e);
-      sEA[r * SW + c] = make_float2(e, e * a);
-      sA2[r * SW + c] = make_float2(a * a, a * a);
-    }
-  }
-  __syncthreads();
-
-  const int r = threadIdx.y;
-  const int rr = r0 + r;
-  if (rr >= p.in_rows) return;
-  const int xs = threadIdx.x * RX;
-  float2 win[NW];
-#pragma unroll
-  for (int j = 0; j < NW; j++) win[j] = sEA[r * SW + xs + j];
-
-  float2* dst = p.planes + b * p.planes_img_stride + (long long)rr * p.Wd + x0 + xs;
+  const int ncb = (p.Wd + C::WCOLS - 1) / C::WCOLS;
+  const int nrb = (p.in_rows + 3) / 4;
+  const int ntask = ncb * nrb * p.B;
+  const int r = lane >> 3, tx = lane & 7;
   const long long pstride = (long long)p.in_rows * p.Wd;
-  const int nvalid = min(RX, p.Wd - (x0 + xs));
+  const bool vec = (p.Wd & 1) == 0;
 
-  for (int pp = 0; pp < p.NP; pp++) {
-    float2 acc[RX];
+  float fv[4][C::NLD];
+  // f for 4 rows x SW columns of a task (mirrored in x at the image edges)
+  auto load_f = [&](int t) {
+    const int x0 = (t % ncb) * C::WCOLS, y0 = ((t / ncb) % nrb) * 4, b = t / (ncb * nrb);
+    const bool xint = (x0 - W >= 0) && (x0 + C::WCOLS + W <= p.Wd);
 #pragma unroll
-    for (int i = 0; i < RX; i++) acc[i] = make_float2(0.f, 0.f);
+    for (int rr = 0; rr < 4; rr++) {
+      const float* src = row_ptr(p, b, p.in_row0 + min(y0 + rr, p.in_rows - 1));
 #pragma unroll
-    for (int j = 0; j < NW; j++) {
-#pragma unroll
-      for (int i = 0; i < RX; i++) {
-        const int m = j - i;                     // tap index, output i, input j
-        if (m >= 0 && m <= 2 * W) acc[i] = f2fma(p.tap2[m], win[j], acc[i]);
+      for (int k = 0; k < C::NLD; k++) {
+        const int c = lane + 32 * k;
+        const int gx = xint ? x0 - W + c : mirror(x0 - W + c, p.Wd);
+        fv[rr][k] = (c < C::SW) ? __ldg(src + gx) : 0.f;
       }
     }
+  };
+  if (blockIdx.x * kRowWarpsPerCta + warp < ntask) load_f(blockIdx.x * kRowWarpsPerCta + warp);
+
+  for (int task = blockIdx.x * kRowWarpsPerCta + warp; task < ntask; task += gridDim.x * kRowWarpsPerCta) {
+    const int cb = task % ncb;
+    const int rb = (task / ncb) % nrb;
+    const int b = task / (ncb * nrb);
+    const int x0 = cb * C::WCOLS, y0 = rb * 4;
+
+    // 1. stage f (loaded during the previous task, see the prefetch below)
 #pragma unroll
-    for (int i = 0; i < RX; i++)
-      if (i < nvalid) dst[i] = acc[i];
-    dst += pstride;
-    if (pp + 1 < p.NP) {
+    for (int rr = 0; rr < 4; rr++) {
 #pragma unroll
-      for (int j = 0; j < NW; j++) win[j] = f2mul(win[j], sA2[r * SW + xs + j]);
+      for (int k = 0; k < C::NLD; k++) {
+        const int c = lane + 32 * k;
+        if (c < C::SW) {
+          float a, e;
+          centre(p, fv[rr][k], a, e);
+          sPsi[rr * C::SWP + C::pad(c)] = make_float2(e, e * a);      // pair 0: e (1, a')
+          sA2[rr * C::SWP + C::pad(c)] = make_float2(a * a, a * a);
+        }
+      }
+    }
+    __syncwarp();
+    // prefetch the next task's f while this task is filtered
+    if (task + gridDim.x * kRowWarpsPerCta < ntask) load_f(task + gridDim.x * kRowWarpsPerCta);
+
+    const float2* wrow = sPsi + r * C::SWP;
+    float2* drow = p.planes + b * p.planes_img_stride + (long long)y0 * p.Wd + x0;
+    for (int pp = 0; pp < p.NP; pp++) {
+      float2 acc[RX];
+#pragma unroll
+      for (int i = 0; i < RX; i++) acc[i] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < C::NW; j++) {
+        const float2 v = wrow[C::pad(RX * tx + j)];
+#pragma unroll
+        for (int i = 0; i < RX; i++) {
+          const int m = j - i;
+          if (m >= 0 && m <= 2 * W) acc[i] = f2fma(make_float2(p.tap[m], p.tap[m]), v, acc[i]);
+        }
+      }
+      // 2. stage the pair, then 4 rows of 128 pairs with 16-byte stores
+#pragma unroll
+      for (int i = 0; i < RX; i++) sO[r * C::OWP + C::pad(RX * tx + i)] = acc[i];
+      __syncwarp();
+#pragma unroll
+      for (int rr = 0; rr < 4; rr++) {
+        if (y0 + rr < p.in_rows) {
+          float2* d = drow + pp * pstride + (long long)rr * p.Wd;
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int c = 2 * lane + 64 * h;
+            const float2 u = sO[rr * C::OWP + C::pad(c)], v = sO[rr * C::OWP + C::pad(c + 1)];
+            if (vec && x0 + c + 1 < p.Wd) {
+              *reinterpret_cast<float4*>(d + c) = make_float4(u.x, u.y, v.x, v.y);
+            } else {
+              if (x0 + c < p.Wd) d[c] = u;
+              if (x0 + c + 1 < p.Wd) d[c + 1] = v;
+            }
+          }
+        }
+      }
+      // 3. next plane pair: psi <- psi a'^2, once per staged element
+      if (pp + 1 < p.NP) {
+        float2 u[4][C::NLD], w[4][C::NLD];       // all loads first, then multiply, then store
+#pragma unroll
+        for (int rr = 0; rr < 4; rr++)
+#pragma unroll
+          for (int k = 0; k < C::NLD; k++) {
+            const int c = min(lane + 32 * k, C::SW - 1);
+            u[rr][k] = sPsi[rr * C::SWP + C::pad(c)];
+            w[rr][k] = sA2[rr * C::SWP + C::pad(c)];
+          }
+#pragma unroll
+        for (int rr = 0; rr < 4; rr++)
+#pragma unroll
+          for (int k = 0; k < C::NLD; k++) {
+            const int c = lane + 32 * k;
+            if (c < C::SW) sPsi[rr * C::SWP + C::pad(c)] = f2mul(u[rr][k], w[rr][k]);
+          }
+      }
+      __syncwarp();
     }
   }
 }
 
 // ------------------------------------------------------------------ K_col (templated W)
+//
+// Persistent, warp-specialised pipeline.  CTA = 1 producer warp + 4 consumer warps.
+// Task: 32 image columns x 32 output rows; consumer warp c owns rows [8c, 8c+8) of the
+// task, lane = column.  A "stage" is one plane pair of one task: the (32 + 2W)-row x
+// 32-column strip of the row-pass buffer that the task's column FIR reads.  The producer
+// fills a 4-deep ring of stage buffers: one TMA 2-D tensor copy per stage for interior
+// strips (cp.async.bulk.tensor, OOB columns zero-filled), one bulk copy per row for strips
+// that need the symmetric extension at the top/bottom edge, and plain loads for odd
+// widths.  full[s] / empty[s] mbarriers hand buffers between producer and consumers, so
+// consumer warps never meet at a CTA barrier.  Consumers run the FIR input-stationary
+// from shared memory (exact tap count) and fold each filtered pair into P and Q
+// (eqs. 8-9) in registers; eq. (10) and the guard are applied at the end of the task.
 
-template <int W, int RY, int CY>
-__global__ void __launch_bounds__(32 * CY) k_col_t(const KParams p) {
-  constexpr int NW = RY + 2 * W;
-  const int b = blockIdx.z;
-  const int x = blockIdx.x * 32 + threadIdx.x;
-  const int y0 = (blockIdx.y * CY + threadIdx.y) * RY;   // first output row, relative
-  if (x >= p.Wd || y0 >= p.out_rows) return;
+constexpr int kColConsumers = 4;
+constexpr int kColStages = 4;
 
-  // Input row j is global row g0 + j, mirrored (eq. 7 symmetric extension).  Interior
-  // windows read consecutive plane-buffer rows; edge windows map each row explicitly.
-  const int g0 = p.out_row0 + y0 - W;
-  const int last = p.out_rows - 1;
-  const bool interior = (g0 >= 0) && (g0 + NW - 1 <= p.H - 1) && (g0 - p.in_row0 >= 0) &&
-                        (g0 + NW - 1 - p.in_row0 < p.in_rows) && (y0 + RY <= p.out_rows);
-  const int jmax = min(RY, p.out_rows - y0) - 1 + 2 * W;   // last input row a stored output uses
+template <int W>
+struct ColCfg {
+  static constexpr int RY = 8;
+  static constexpr int TROWS = kColConsumers * RY;     // output rows per task
+  static constexpr int NJ = TROWS + 2 * W;             // strip rows per stage
+  static constexpr int NW = RY + 2 * W;
+  static constexpr int BUF = NJ * 32;                  // float2 per stage buffer
+  static constexpr int BUFB = BUF * 8;
+  static constexpr int SMEM = kColStages * BUFB + 2 * kColStages * 8 + 128;
+};
 
-  float a2[RY];
-  float2 pw[RY], P2[RY], Q2[RY];
-  float vpy[RY];
-  float fo[RY];
-#pragma unroll
-  for (int i = 0; i < RY; i++) {
-    const int yy = min(y0 + i, last);
-    float a, e;
-    fo[i] = __ldg(row_ptr(p, b, p.out_row0 + yy) + x);
-    centre(p, fo[i], a, e);
-    a2[i] = a * a;
-    pw[i] = make_float2(1.f, a);                  // (G'_0, G'_1) = (1, a')
-    P2[i] = make_float2(0.f, 0.f);
-    Q2[i] = make_float2(0.f, 0.f);
-    vpy[i] = 0.f;                                 // v_{-1} = 0
-  }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(s) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(s),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, unsigned long long* bar) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(s),
+               "l"(gmem), "r"(bytes), "r"(b)
+               : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* smem, const CUtensorMap* map, int c0, int c1, unsigned long long* bar) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(s),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(b)
+      : "memory");
+}
 
-  const float2* base = p.planes + b * p.planes_img_stride + x;
+template <int W>
+__global__ void __launch_bounds__(32 * (kColConsumers + 1), 3)
+    k_col_t(const __grid_constant__ CUtensorMap tmap, const KParams p) {
+  using C = ColCfg<W>;
+  constexpr int RY = C::RY;
+  extern __shared__ float4 smem_col[];
+  char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_col) + 127) & ~uintptr_t(127));
+  float2* sB = reinterpret_cast<float2*>(base);                                         // [S][NJ][32]
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(base + kColStages * C::BUFB);
+  unsigned long long* empty = full + kColStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const int ncb = (p.Wd + 31) / 32;
+  const int nrb = (p.out_rows + C::TROWS - 1) / C::TROWS;
+  const int ntask = ncb * nrb * p.B;
   const long long pstride = (long long)p.in_rows * p.Wd;
-  for (int pp = 0; pp < p.NP; pp++) {
-    float2 acc[RY];
-#pragma unroll
-    for (int i = 0; i < RY; i++) acc[i] = make_float2(0.f, 0.f);
-    const float2* pl = base + pp * pstride;
-    if (interior) {
-      const float2* q = pl + (long long)(g0 - p.in_row0) * p.Wd;
-#pragma unroll
-      for (int j = 0; j < NW; j++) {
-        const float2 v = __ldg(q + (long long)j * p.Wd);
-#pragma unroll
-        for (int i = 0; i < RY; i++) {
-          const int m = j - i;
-          if (m >= 0 && m <= 2 * W) acc[i] = f2fma(p.tap2[m], v, acc[i]);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < NW; j++) {
-        // rows feeding only outputs beyond out_rows are clamped (results not stored)
-        int q = mirror(g0 + min(j, jmax), p.H) - p.in_row0;
-        q = min(max(q, 0), p.in_rows - 1);
-        const float2 v = __ldg(pl + (long long)q * p.Wd);
-#pragma unroll
-        for (int i = 0; i < RY; i++) {
-          const int m = j - i;
-          if (m >= 0 && m <= 2 * W) acc[i] = f2fma(p.tap2[m], v, acc[i]);
+  const int last = p.out_rows - 1;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kColStages; i++) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kColConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kColConsumers) {
+    // ------------------------------------------------ producer warp
+    const bool tma_ok = (p.Wd & 1) == 0;          // 16-byte global row stride
+    int k = 0;
+    for (int task = blockIdx.x; task < ntask; task += gridDim.x) {
+      const int rb = task % nrb;
+      const int cb = (task / nrb) % ncb;
+      const int b = task / (nrb * ncb);
+      const int x0 = cb * 32, y0 = rb * C::TROWS;
+      const int g0 = p.out_row0 + y0 - W;
+      const int jmax = min(C::TROWS, p.out_rows - y0) - 1 + 2 * W;
+      const bool interior = (g0 >= 0) && (g0 + C::NJ - 1 <= p.H - 1) && (g0 - p.in_row0 >= 0) &&
+                            (g0 + C::NJ - 1 - p.in_row0 < p.in_rows) && (jmax == C::NJ - 1);
+      for (int pp = 0; pp < p.NP; pp++, k++) {
+        const int s = k % kColStages;
+        if (k >= kColStages) mbar_wait(&empty[s], ((k / kColStages) - 1) & 1);
+        float2* dst = sB + s * C::BUF;
+        if (tma_ok && interior) {
+          if (lane == 0) {
+            mbar_expect_tx(&full[s], C::BUFB);
+            tma_2d(dst, &tmap, x0, (b * p.NP + pp) * p.in_rows + (g0 - p.in_row0), &full[s]);
+          }
+        } else if (tma_ok && x0 + 32 <= p.Wd) {
+          // symmetric extension at the top / bottom: one bulk copy per strip row
+          if (lane == 0) mbar_expect_tx(&full[s], C::BUFB);
+          __syncwarp();
+          const float2* pl = p.planes + b * p.planes_img_stride + pp * pstride + x0;
+          for (int j = lane; j < C::NJ; j += 32) {
+            int q = mirror(g0 + min(j, jmax), p.H) - p.in_row0;
+            q = min(max(q, 0), p.in_rows - 1);
+            bulk_g2s(dst + j * 32, pl + (long long)q * p.Wd, 256, &full[s]);
+          }
+        } else {
+          // odd width or right-edge strip at an edge row: plain loads
+          const float2* pl = p.planes + b * p.planes_img_stride + pp * pstride + x0;
+          for (int j = 0; j < C::NJ; j++) {
+            int q = mirror(g0 + min(j, jmax), p.H) - p.in_row0;
+            q = min(max(q, 0), p.in_rows - 1);
+            dst[j * 32 + lane] = (x0 + lane < p.Wd) ? pl[(long long)q * p.Wd + lane] : make_float2(0.f, 0.f);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[s]);
         }
       }
     }
-    // eqs. (8)-(9): v_n = chat_n G'_n;  Q += v_n Fbar_n;  P += v_{n-1} Fbar_n
-    const float2 c2 = p.chat2[pp];
+    return;
+  }
+
+  // ------------------------------------------------ consumer warps
+  const int seg = warp;
+  int k = 0;
+  for (int task = blockIdx.x; task < ntask; task += gridDim.x) {
+    const int rb = task % nrb;
+    const int cb = (task / nrb) % ncb;
+    const int b = task / (nrb * ncb);
+    const int x0 = cb * 32, y0 = rb * C::TROWS;
+    const int x = x0 + lane;
+
+    float av[RY], P[RY], Q[RY], vpy[RY], pwx[RY];
 #pragma unroll
     for (int i = 0; i < RY; i++) {
-      const float2 v2 = f2mul(c2, pw[i]);
-      Q2[i] = f2fma(v2, acc[i], Q2[i]);
-      P2[i] = f2fma(make_float2(vpy[i], v2.x), acc[i], P2[i]);
-      vpy[i] = v2.y;
-      pw[i] = f2mul(pw[i], make_float2(a2[i], a2[i]));
+      const int yy = min(y0 + RY * seg + i, last);
+      float a, e;
+      centre(p, (x < p.Wd) ? __ldg(row_ptr(p, b, p.out_row0 + yy) + x) : 0.f, a, e);
+      av[i] = a;
+      pwx[i] = 1.f;            // G'_{2p} = a'^{2p}
+      P[i] = 0.f;
+      Q[i] = 0.f;
+      vpy[i] = 0.f;            // v_{-1} = 0
     }
-  }
 
-  float* out = p.out + b * p.out_img_stride + x;
+    for (int pp = 0; pp < p.NP; pp++, k++) {
+      const int s = k % kColStages;
+      mbar_wait(&full[s], (k / kColStages) & 1);
+      const float2* col = sB + s * C::BUF + (RY * seg) * 32 + lane;
+      float2 acc[RY];
 #pragma unroll
-  for (int i = 0; i < RY; i++) {
-    if (y0 + i > last) break;
-    const float Q = Q2[i].x + Q2[i].y;
-    const float P = P2[i].x + P2[i].y;
-    float o;
-    if (Q > 0.f && isfinite(Q) && isfinite(P)) {
-      o = p.t_c + p.t_h * __fdividef(P, Q);       // eq. (10) + uncentring
-      if (!isfinite(o)) o = p.t_c + p.t_h * (P / Q);
-    } else {
-      o = fminf(fmaxf(fo[i], p.L), p.U);          // guard (R8)
-      if (p.fallback) atomicAdd(p.fallback, 1ull);
+      for (int i = 0; i < RY; i++) acc[i] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < C::NW; j++) {
+        const float2 v = col[j * 32];
+#pragma unroll
+        for (int i = 0; i < RY; i++) {
+          const int m = j - i;
+          if (m >= 0 && m <= 2 * W) acc[i] = f2fma(make_float2(p.tap[m], p.tap[m]), v, acc[i]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);     // strip no longer needed by this warp
+      // eqs. (8)-(9) with v_n = chat_n G'_n:  Q += v_n Fbar_n,  P += v_{n-1} Fbar_n
+      const float2 c2 = p.chat2[pp];
+#pragma unroll
+      for (int i = 0; i < RY; i++) {
+        const float v0 = c2.x * pwx[i];
+        const float v1 = c2.y * (pwx[i] * av[i]);
+        Q[i] = fmaf(v0, acc[i].x, Q[i]);
+        Q[i] = fmaf(v1, acc[i].y, Q[i]);
+        P[i] = fmaf(vpy[i], acc[i].x, P[i]);
+        P[i] = fmaf(v0, acc[i].y, P[i]);
+        vpy[i] = v1;
+        pwx[i] *= av[i] * av[i];
+      }
     }
-    out[(long long)(y0 + i) * p.Wd] = o;
+
+    if (x < p.Wd) {
+      float* out = p.out + b * p.out_img_stride + x;
+#pragma unroll
+      for (int i = 0; i < RY; i++) {
+        const int yy = y0 + RY * seg + i;
+        if (yy > last) break;
+        const float Qi = Q[i], Pi = P[i];
+        float o;
+        if (Qi > 0.f && isfinite(Qi) && isfinite(Pi)) {
+          o = p.t_c + p.t_h * (Pi / Qi);                 // eq. (10) + uncentring
+        } else {                                          // guard (R8)
+          o = fminf(fmaxf(av[i] * p.t_h + p.t_c, p.L), p.U);
+          if (p.fallback) atomicAdd(p.fallback, 1ull);
+        }
+        out[(long long)yy * p.Wd] = o;
+      }
+    }
   }
 }
 
@@ -267,24 +477,58 @@ __global__ void __launch_bounds__(256) k_col_rt(const KParams p) {
 
 namespace {
 
+// TMA descriptor of the row-pass buffer seen as a 2-D tensor of 8-byte elements:
+// [B * NP * in_rows rows][Wd columns], box = 32 columns x `box_rows` rows.
+bool make_plane_map(CUtensorMap* map, const KParams& p, int box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if ((p.Wd & 1) != 0) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)p.Wd, (cuuint64_t)p.B * p.NP * p.in_rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)p.Wd * 8};
+  const cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_INT64, 2, (void*)p.planes, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int W>
 cudaError_t launch_t(const KParams& p, cudaStream_t s) {
-  constexpr int RX = (W <= 16) ? 16 : 8;
-  constexpr int TXT = 8, TY = 16;
-  constexpr int RY = 8, CY = 8;
-  constexpr int TX = TXT * RX;
-  const size_t smem = (size_t)TY * (TX + 2 * W) * 16;
-  auto kr = k_row_t<W, RX, TXT, TY>;
-  cudaError_t e = cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  dim3 gr((p.Wd + TX - 1) / TX, (p.in_rows + TY - 1) / TY, p.B);
+  using CR = RowCfg<W>;
+  using CC = ColCfg<W>;
+  const size_t smem_r = (size_t)kRowWarpsPerCta * CR::SMEM_WARP;
+  const size_t smem_c = (size_t)CC::SMEM;
+  auto kr = k_row_t<W>;
+  auto kc = k_col_t<W>;
+  static int occ_r = 0, occ_c = 0;       // per instantiation, computed once
+  if (occ_r == 0) {
+    cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r);
+    cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_r, kr, 32 * kRowWarpsPerCta, smem_r);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, kc, 32 * (kColConsumers + 1), smem_c);
+    occ_r = std::max(occ_r, 1);
+    occ_c = std::max(occ_c, 1);
+  }
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  if ((p.Wd & 1) == 0 && !make_plane_map(&map, p, CC::NJ)) return cudaErrorInvalidValue;
+  const long long ntr = (long long)((p.Wd + CR::WCOLS - 1) / CR::WCOLS) * ((p.in_rows + 3) / 4) * p.B;
+  const long long gr = std::min<long long>((ntr + kRowWarpsPerCta - 1) / kRowWarpsPerCta, (long long)occ_r * p.num_sms);
+  const long long ntc = (long long)((p.Wd + 31) / 32) * ((p.out_rows + CC::TROWS - 1) / CC::TROWS) * p.B;
+  const long long gc = std::min<long long>(ntc, (long long)occ_c * p.num_sms);
   if (p.ev[0]) cudaEventRecord(p.ev[0], s);
-  kr<<<gr, dim3(TXT, TY), smem, s>>>(p);
-  e = cudaGetLastError();
+  kr<<<(unsigned)gr, 32 * kRowWarpsPerCta, smem_r, s>>>(p);
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (p.ev[1]) cudaEventRecord(p.ev[1], s);
-  dim3 gc((p.Wd + 31) / 32, (p.out_rows + RY * CY - 1) / (RY * CY), p.B);
-  k_col_t<W, RY, CY><<<gc, dim3(32, CY), 0, s>>>(p);
+  kc<<<(unsigned)gc, 32 * (kColConsumers + 1), smem_c, s>>>(map, p);
   e = cudaGetLastError();
   if (p.ev[2]) cudaEventRecord(p.ev[2], s);
   return e;

@@ -37,7 +37,8 @@ struct KParams {
   int out_row0, out_rows; // global rows written
   Seg seg[3];             // input rows (see gc_filter_window)
   long long seg_img_stride;   // elements between consecutive images in every segment
-  float2* planes;         // [B][NP][in_rows][Wd] pairs (row pass output)
+  float2* planes;         // row pass output [B][NP][in_rows][Wd] (plane pairs, row-major)
+  int in_pitch;           // unused (reserved)
   long long planes_img_stride; // float2 elements per image
   float* out;             // [B][out_rows][Wd]
   long long out_img_stride;
@@ -50,7 +51,9 @@ struct KParams {
   const float2* taps_g;   // (k_m, k_m), m = 0..2R, in global memory (runtime-W kernels)
   cudaEvent_t ev[3];      // optional timing events (host side only; not read on device)
   float2 chat2[kMaxPairs];         // (chat_{2p}, chat_{2p+1}), zero beyond N
-  float2 tap2[2 * kMaxTemplW + 1]; // (k_m, k_m), m = 0..2R (unrolled kernels)
+  float tap[2 * kMaxTemplW + 1];   // k_m, m = 0..2R (unrolled kernels; FFMA2 scalar broadcast)
+  int ctas_per_sm;                 // persistent-grid sizing (host side)
+  int num_sms;
 };
 
 // Launch the two-pass FIR pipeline (row pass + column pass with recombination) on

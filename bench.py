@@ -45,6 +45,7 @@ def _args():
     a.add_argument("--sigma-r", type=float, default=None, help="override (default: stated)")
     a.add_argument("--impl", default="ours", choices=["ours", "reference"])
     a.add_argument("--no-e2e", action="store_true")
+    a.add_argument("--batch", type=int, default=None, help="override the batch size (profiling only)")
     a.add_argument("--no-cpu-baseline", action="store_true")
     return a.parse_args()
 
@@ -191,6 +192,9 @@ def main():
 
     # ---- inputs resident in HBM before the timed region
     comm = None
+    if args.batch is not None:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, batch=args.batch)
     if cfg.name == "c4":
         per = cfg.batch // ws
         imgs = np.stack([config_image(cfg, index=rank * per + i) for i in range(per)])

@@ -127,8 +127,10 @@ gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) 
   const size_t plane_elems = (size_t)k.NP * k.in_rows * k.Wd;
   float2* planes = nullptr;
   float2* taps_dev = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&planes, plane_elems * k.B * sizeof(float2), s);
+  // plane buffer + 256 bytes of task counters at its end
+  cudaError_t e = cudaMallocAsync((void**)&planes, plane_elems * k.B * sizeof(float2) + 256, s);
   if (e != cudaSuccess) return cuda_status(e);
+  k.counters = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(planes) + plane_elems * k.B * sizeof(float2));
   if (k.R > kMaxTemplW) {
     e = cudaMallocAsync((void**)&taps_dev, taps_host.size() * sizeof(float2), s);
     if (e == cudaSuccess)

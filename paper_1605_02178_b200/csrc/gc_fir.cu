@@ -38,7 +38,7 @@ namespace gc {
 // compile-time tap indices), and each filtered pair is written as full rows with
 // 16-byte stores after a shared-memory transpose-free staging.
 
-constexpr int kRowWarpsPerCta = 4;
+constexpr int kRowWarpsPerCta = 1;
 
 template <int W>
 struct RowCfg {
@@ -53,125 +53,118 @@ struct RowCfg {
   static constexpr int SWP = SWP0 + (24 - SWP0 % 16) % 16;   // row stride = 8 (mod 16) pairs
   static constexpr int OWP0 = WCOLS + (WCOLS >> 4) + 1;
   static constexpr int OWP = OWP0 + (24 - OWP0 % 16) % 16;
-  static constexpr int SMEM_WARP = (2 * 4 * SWP + 4 * OWP) * 8;
+  static constexpr int A2W = SW + 1;                         // scalar a'^2 row stride
+  static constexpr int SMEM_WARP = (4 * SWP + 4 * OWP) * 8 + 4 * A2W * 4;
 };
 
 template <int W>
-__global__ void __launch_bounds__(32 * kRowWarpsPerCta, 4) k_row_t(const KParams p) {
+__global__ void __launch_bounds__(32 * kRowWarpsPerCta, 16) k_row_t(const KParams p, unsigned* col_task_ctr) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *col_task_ctr = 0u;   // consumed by k_col_t (stream-ordered)
   using C = RowCfg<W>;
   constexpr int RX = C::RX;
   extern __shared__ float4 smem_row[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float2* sPsi = reinterpret_cast<float2*>(smem_row) + warp * (C::SMEM_WARP / 8);  // [4][SWP] current pair
-  float2* sA2 = sPsi + 4 * C::SWP;                                                   // [4][SWP] (a'^2, a'^2)
-  float2* sO = sA2 + 4 * C::SWP;                                                     // [4][OWP]
+  const int lane = threadIdx.x & 31;
+  float2* sPsi = reinterpret_cast<float2*>(smem_row);        // [4][SWP] current plane pair
+  float2* sO = sPsi + 4 * C::SWP;                              // [4][OWP]
+  float* sA2 = reinterpret_cast<float*>(sO + 4 * C::OWP);      // [4][A2W] a'^2
 
   const int ncb = (p.Wd + C::WCOLS - 1) / C::WCOLS;
   const int nrb = (p.in_rows + 3) / 4;
-  const int ntask = ncb * nrb * p.B;
   const int r = lane >> 3, tx = lane & 7;
   const long long pstride = (long long)p.in_rows * p.Wd;
   const bool vec = (p.Wd & 1) == 0;
 
+  const int task = blockIdx.x;
+  const int cb = task % ncb;
+  const int rb = (task / ncb) % nrb;
+  const int b = task / (ncb * nrb);
+  const int x0 = cb * C::WCOLS, y0 = rb * 4;
+  const bool xint = (x0 - W >= 0) && (x0 + C::WCOLS + W <= p.Wd);
+
+  // 1. stage f: 4 rows x SW columns (mirrored in x at the image edges), loads first
   float fv[4][C::NLD];
-  // f for 4 rows x SW columns of a task (mirrored in x at the image edges)
-  auto load_f = [&](int t) {
-    const int x0 = (t % ncb) * C::WCOLS, y0 = ((t / ncb) % nrb) * 4, b = t / (ncb * nrb);
-    const bool xint = (x0 - W >= 0) && (x0 + C::WCOLS + W <= p.Wd);
 #pragma unroll
-    for (int rr = 0; rr < 4; rr++) {
-      const float* src = row_ptr(p, b, p.in_row0 + min(y0 + rr, p.in_rows - 1));
+  for (int rr = 0; rr < 4; rr++) {
+    const float* src = row_ptr(p, b, p.in_row0 + min(y0 + rr, p.in_rows - 1));
 #pragma unroll
-      for (int k = 0; k < C::NLD; k++) {
-        const int c = lane + 32 * k;
-        const int gx = xint ? x0 - W + c : mirror(x0 - W + c, p.Wd);
-        fv[rr][k] = (c < C::SW) ? __ldg(src + gx) : 0.f;
+    for (int k = 0; k < C::NLD; k++) {
+      const int c = lane + 32 * k;
+      const int gx = xint ? x0 - W + c : mirror(x0 - W + c, p.Wd);
+      fv[rr][k] = (c < C::SW) ? __ldg(src + gx) : 0.f;
+    }
+  }
+#pragma unroll
+  for (int rr = 0; rr < 4; rr++) {
+#pragma unroll
+    for (int k = 0; k < C::NLD; k++) {
+      const int c = lane + 32 * k;
+      if (c < C::SW) {
+        float a, e;
+        centre(p, fv[rr][k], a, e);
+        sPsi[rr * C::SWP + C::pad(c)] = make_float2(e, e * a);      // pair 0: e (1, a')
+        sA2[rr * C::A2W + c] = a * a;
       }
     }
-  };
-  if (blockIdx.x * kRowWarpsPerCta + warp < ntask) load_f(blockIdx.x * kRowWarpsPerCta + warp);
+  }
+  __syncwarp();
 
-  for (int task = blockIdx.x * kRowWarpsPerCta + warp; task < ntask; task += gridDim.x * kRowWarpsPerCta) {
-    const int cb = task % ncb;
-    const int rb = (task / ncb) % nrb;
-    const int b = task / (ncb * nrb);
-    const int x0 = cb * C::WCOLS, y0 = rb * 4;
-
-    // 1. stage f (loaded during the previous task, see the prefetch below)
+  const float2* wrow = sPsi + r * C::SWP;
+  float2* drow = p.planes + b * p.planes_img_stride + (long long)y0 * p.Wd + x0;
+  for (int pp = 0; pp < p.NP; pp++) {
+    float2 acc[RX];
+#pragma unroll
+    for (int i = 0; i < RX; i++) acc[i] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < C::NW; j++) {
+      const float2 v = wrow[C::pad(RX * tx + j)];
+#pragma unroll
+      for (int i = 0; i < RX; i++) {
+        const int m = j - i;
+        if (m >= 0 && m <= 2 * W) acc[i] = f2fma(make_float2(p.tap[m], p.tap[m]), v, acc[i]);
+      }
+    }
+    // 2. stage the pair, then 4 rows of 128 pairs with 16-byte stores
+#pragma unroll
+    for (int i = 0; i < RX; i++) sO[r * C::OWP + C::pad(RX * tx + i)] = acc[i];
+    __syncwarp();
 #pragma unroll
     for (int rr = 0; rr < 4; rr++) {
+      if (y0 + rr < p.in_rows) {
+        float2* d = drow + pp * pstride + (long long)rr * p.Wd;
 #pragma unroll
-      for (int k = 0; k < C::NLD; k++) {
-        const int c = lane + 32 * k;
-        if (c < C::SW) {
-          float a, e;
-          centre(p, fv[rr][k], a, e);
-          sPsi[rr * C::SWP + C::pad(c)] = make_float2(e, e * a);      // pair 0: e (1, a')
-          sA2[rr * C::SWP + C::pad(c)] = make_float2(a * a, a * a);
+        for (int h = 0; h < 2; h++) {
+          const int c = 2 * lane + 64 * h;
+          const float2 u = sO[rr * C::OWP + C::pad(c)], v = sO[rr * C::OWP + C::pad(c + 1)];
+          if (vec && x0 + c + 1 < p.Wd) {
+            *reinterpret_cast<float4*>(d + c) = make_float4(u.x, u.y, v.x, v.y);
+          } else {
+            if (x0 + c < p.Wd) d[c] = u;
+            if (x0 + c + 1 < p.Wd) d[c + 1] = v;
+          }
         }
       }
+    }
+    // 3. next plane pair: psi <- psi a'^2, once per staged element (loads, then stores)
+    if (pp + 1 < p.NP) {
+      float2 u[4][C::NLD];
+      float w[4][C::NLD];
+#pragma unroll
+      for (int rr = 0; rr < 4; rr++)
+#pragma unroll
+        for (int k = 0; k < C::NLD; k++) {
+          const int c = min(lane + 32 * k, C::SW - 1);
+          u[rr][k] = sPsi[rr * C::SWP + C::pad(c)];
+          w[rr][k] = sA2[rr * C::A2W + c];
+        }
+#pragma unroll
+      for (int rr = 0; rr < 4; rr++)
+#pragma unroll
+        for (int k = 0; k < C::NLD; k++) {
+          const int c = lane + 32 * k;
+          if (c < C::SW) sPsi[rr * C::SWP + C::pad(c)] = f2mul(u[rr][k], make_float2(w[rr][k], w[rr][k]));
+        }
     }
     __syncwarp();
-    // prefetch the next task's f while this task is filtered
-    if (task + gridDim.x * kRowWarpsPerCta < ntask) load_f(task + gridDim.x * kRowWarpsPerCta);
-
-    const float2* wrow = sPsi + r * C::SWP;
-    float2* drow = p.planes + b * p.planes_img_stride + (long long)y0 * p.Wd + x0;
-    for (int pp = 0; pp < p.NP; pp++) {
-      float2 acc[RX];
-#pragma unroll
-      for (int i = 0; i < RX; i++) acc[i] = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int j = 0; j < C::NW; j++) {
-        const float2 v = wrow[C::pad(RX * tx + j)];
-#pragma unroll
-        for (int i = 0; i < RX; i++) {
-          const int m = j - i;
-          if (m >= 0 && m <= 2 * W) acc[i] = f2fma(make_float2(p.tap[m], p.tap[m]), v, acc[i]);
-        }
-      }
-      // 2. stage the pair, then 4 rows of 128 pairs with 16-byte stores
-#pragma unroll
-      for (int i = 0; i < RX; i++) sO[r * C::OWP + C::pad(RX * tx + i)] = acc[i];
-      __syncwarp();
-#pragma unroll
-      for (int rr = 0; rr < 4; rr++) {
-        if (y0 + rr < p.in_rows) {
-          float2* d = drow + pp * pstride + (long long)rr * p.Wd;
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            const int c = 2 * lane + 64 * h;
-            const float2 u = sO[rr * C::OWP + C::pad(c)], v = sO[rr * C::OWP + C::pad(c + 1)];
-            if (vec && x0 + c + 1 < p.Wd) {
-              *reinterpret_cast<float4*>(d + c) = make_float4(u.x, u.y, v.x, v.y);
-            } else {
-              if (x0 + c < p.Wd) d[c] = u;
-              if (x0 + c + 1 < p.Wd) d[c + 1] = v;
-            }
-          }
-        }
-      }
-      // 3. next plane pair: psi <- psi a'^2, once per staged element
-      if (pp + 1 < p.NP) {
-        float2 u[4][C::NLD], w[4][C::NLD];       // all loads first, then multiply, then store
-#pragma unroll
-        for (int rr = 0; rr < 4; rr++)
-#pragma unroll
-          for (int k = 0; k < C::NLD; k++) {
-            const int c = min(lane + 32 * k, C::SW - 1);
-            u[rr][k] = sPsi[rr * C::SWP + C::pad(c)];
-            w[rr][k] = sA2[rr * C::SWP + C::pad(c)];
-          }
-#pragma unroll
-        for (int rr = 0; rr < 4; rr++)
-#pragma unroll
-          for (int k = 0; k < C::NLD; k++) {
-            const int c = lane + 32 * k;
-            if (c < C::SW) sPsi[rr * C::SWP + C::pad(c)] = f2mul(u[rr][k], w[rr][k]);
-          }
-      }
-      __syncwarp();
-    }
   }
 }
 
@@ -190,7 +183,7 @@ __global__ void __launch_bounds__(32 * kRowWarpsPerCta, 4) k_row_t(const KParams
 // (eqs. 8-9) in registers; eq. (10) and the guard are applied at the end of the task.
 
 constexpr int kColConsumers = 4;
-constexpr int kColStages = 4;
+constexpr int kColStages = 3;
 
 template <int W>
 struct ColCfg {
@@ -200,7 +193,7 @@ struct ColCfg {
   static constexpr int NW = RY + 2 * W;
   static constexpr int BUF = NJ * 32;                  // float2 per stage buffer
   static constexpr int BUFB = BUF * 8;
-  static constexpr int SMEM = kColStages * BUFB + 2 * kColStages * 8 + 128;
+  static constexpr int SMEM = kColStages * BUFB + 2 * kColStages * 8 + kColStages * 4 + 128;
 };
 
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
@@ -245,7 +238,7 @@ __device__ __forceinline__ void tma_2d(void* smem, const CUtensorMap* map, int c
 
 template <int W>
 __global__ void __launch_bounds__(32 * (kColConsumers + 1), 3)
-    k_col_t(const __grid_constant__ CUtensorMap tmap, const KParams p) {
+    k_col_t(const __grid_constant__ CUtensorMap tmap, const KParams p, unsigned* task_ctr) {
   using C = ColCfg<W>;
   constexpr int RY = C::RY;
   extern __shared__ float4 smem_col[];
@@ -253,6 +246,7 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 3)
   float2* sB = reinterpret_cast<float2*>(base);                                         // [S][NJ][32]
   unsigned long long* full = reinterpret_cast<unsigned long long*>(base + kColStages * C::BUFB);
   unsigned long long* empty = full + kColStages;
+  int* stage_task = reinterpret_cast<int*>(empty + kColStages);                        // [S]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   const int ncb = (p.Wd + 31) / 32;
@@ -271,10 +265,15 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 3)
   __syncthreads();
 
   if (warp == kColConsumers) {
-    // ------------------------------------------------ producer warp
+    // ------------------------------------------------ producer warp: fetch tasks dynamically,
+    // fill stage buffers (one stage = one plane pair of one task), tag each with its task
     const bool tma_ok = (p.Wd & 1) == 0;          // 16-byte global row stride
     int k = 0;
-    for (int task = blockIdx.x; task < ntask; task += gridDim.x) {
+    for (;;) {
+      int task = 0;
+      if (lane == 0) task = (int)atomicAdd(task_ctr, 1u);
+      task = __shfl_sync(0xffffffffu, task, 0);
+      const bool done = task >= ntask;
       const int rb = task % nrb;
       const int cb = (task / nrb) % ncb;
       const int b = task / (nrb * ncb);
@@ -283,11 +282,16 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 3)
       const int jmax = min(C::TROWS, p.out_rows - y0) - 1 + 2 * W;
       const bool interior = (g0 >= 0) && (g0 + C::NJ - 1 <= p.H - 1) && (g0 - p.in_row0 >= 0) &&
                             (g0 + C::NJ - 1 - p.in_row0 < p.in_rows) && (jmax == C::NJ - 1);
-      for (int pp = 0; pp < p.NP; pp++, k++) {
+      const int npairs = done ? 1 : p.NP;
+      for (int pp = 0; pp < npairs; pp++, k++) {
         const int s = k % kColStages;
         if (k >= kColStages) mbar_wait(&empty[s], ((k / kColStages) - 1) & 1);
+        if (lane == 0) stage_task[s] = done ? -1 : task;
         float2* dst = sB + s * C::BUF;
-        if (tma_ok && interior) {
+        if (done) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[s]);   // sentinel: no more tasks
+        } else if (tma_ok && interior) {
           if (lane == 0) {
             mbar_expect_tx(&full[s], C::BUFB);
             tma_2d(dst, &tmap, x0, (b * p.NP + pp) * p.in_rows + (g0 - p.in_row0), &full[s]);
@@ -314,67 +318,75 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 3)
           if (lane == 0) mbar_arrive(&full[s]);
         }
       }
+      if (done) break;
     }
     return;
   }
 
   // ------------------------------------------------ consumer warps
   const int seg = warp;
-  int k = 0;
-  for (int task = blockIdx.x; task < ntask; task += gridDim.x) {
-    const int rb = task % nrb;
-    const int cb = (task / nrb) % ncb;
-    const int b = task / (nrb * ncb);
-    const int x0 = cb * 32, y0 = rb * C::TROWS;
-    const int x = x0 + lane;
-
-    float av[RY], P[RY], Q[RY], vpy[RY], pwx[RY];
-#pragma unroll
-    for (int i = 0; i < RY; i++) {
-      const int yy = min(y0 + RY * seg + i, last);
-      float a, e;
-      centre(p, (x < p.Wd) ? __ldg(row_ptr(p, b, p.out_row0 + yy) + x) : 0.f, a, e);
-      av[i] = a;
-      pwx[i] = 1.f;            // G'_{2p} = a'^{2p}
-      P[i] = 0.f;
-      Q[i] = 0.f;
-      vpy[i] = 0.f;            // v_{-1} = 0
-    }
-
-    for (int pp = 0; pp < p.NP; pp++, k++) {
-      const int s = k % kColStages;
-      mbar_wait(&full[s], (k / kColStages) & 1);
-      const float2* col = sB + s * C::BUF + (RY * seg) * 32 + lane;
-      float2 acc[RY];
-#pragma unroll
-      for (int i = 0; i < RY; i++) acc[i] = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int j = 0; j < C::NW; j++) {
-        const float2 v = col[j * 32];
-#pragma unroll
-        for (int i = 0; i < RY; i++) {
-          const int m = j - i;
-          if (m >= 0 && m <= 2 * W) acc[i] = f2fma(make_float2(p.tap[m], p.tap[m]), v, acc[i]);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);     // strip no longer needed by this warp
-      // eqs. (8)-(9) with v_n = chat_n G'_n:  Q += v_n Fbar_n,  P += v_{n-1} Fbar_n
-      const float2 c2 = p.chat2[pp];
+  float fo[RY], av[RY], P[RY], Q[RY], vpy[RY], pwx[RY];
+  int b = 0, x = 0, y0 = 0;
+  for (int k = 0;; k++) {
+    const int s = k % kColStages;
+    mbar_wait(&full[s], (k / kColStages) & 1);
+    const int task = stage_task[s];
+    if (task < 0) break;
+    const int pp = k % p.NP;                       // stages arrive in (task, pair) order
+    if (pp == 0) {
+      const int rb = task % nrb;
+      const int cb = (task / nrb) % ncb;
+      b = task / (nrb * ncb);
+      y0 = rb * C::TROWS;
+      x = cb * 32 + lane;
+      // issue the loads of f now, use them after this pair's FIR (latency overlapped)
 #pragma unroll
       for (int i = 0; i < RY; i++) {
-        const float v0 = c2.x * pwx[i];
-        const float v1 = c2.y * (pwx[i] * av[i]);
-        Q[i] = fmaf(v0, acc[i].x, Q[i]);
-        Q[i] = fmaf(v1, acc[i].y, Q[i]);
-        P[i] = fmaf(vpy[i], acc[i].x, P[i]);
-        P[i] = fmaf(v0, acc[i].y, P[i]);
-        vpy[i] = v1;
-        pwx[i] *= av[i] * av[i];
+        const int yy = min(y0 + RY * seg + i, last);
+        fo[i] = (x < p.Wd) ? __ldg(row_ptr(p, b, p.out_row0 + yy) + x) : 0.f;
       }
     }
-
-    if (x < p.Wd) {
+    const float2* col = sB + s * C::BUF + (RY * seg) * 32 + lane;
+    float2 acc[RY];
+#pragma unroll
+    for (int i = 0; i < RY; i++) acc[i] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < C::NW; j++) {
+      const float2 v = col[j * 32];
+#pragma unroll
+      for (int i = 0; i < RY; i++) {
+        const int m = j - i;
+        if (m >= 0 && m <= 2 * W) acc[i] = f2fma(make_float2(p.tap[m], p.tap[m]), v, acc[i]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);       // strip no longer needed by this warp
+    if (pp == 0) {
+#pragma unroll
+      for (int i = 0; i < RY; i++) {
+        float a, e;
+        centre(p, fo[i], a, e);
+        av[i] = a;
+        pwx[i] = 1.f;          // G'_{2p} = a'^{2p}
+        P[i] = 0.f;
+        Q[i] = 0.f;
+        vpy[i] = 0.f;          // v_{-1} = 0
+      }
+    }
+    // eqs. (8)-(9) with v_n = chat_n G'_n:  Q += v_n Fbar_n,  P += v_{n-1} Fbar_n
+    const float2 c2 = p.chat2[pp];
+#pragma unroll
+    for (int i = 0; i < RY; i++) {
+      const float v0 = c2.x * pwx[i];
+      const float v1 = c2.y * (pwx[i] * av[i]);
+      Q[i] = fmaf(v0, acc[i].x, Q[i]);
+      Q[i] = fmaf(v1, acc[i].y, Q[i]);
+      P[i] = fmaf(vpy[i], acc[i].x, P[i]);
+      P[i] = fmaf(v0, acc[i].y, P[i]);
+      vpy[i] = v1;
+      pwx[i] *= av[i] * av[i];
+    }
+    if (pp == p.NP - 1 && x < p.Wd) {
       float* out = p.out + b * p.out_img_stride + x;
 #pragma unroll
       for (int i = 0; i < RY; i++) {
@@ -385,7 +397,7 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 3)
         if (Qi > 0.f && isfinite(Qi) && isfinite(Pi)) {
           o = p.t_c + p.t_h * (Pi / Qi);                 // eq. (10) + uncentring
         } else {                                          // guard (R8)
-          o = fminf(fmaxf(av[i] * p.t_h + p.t_c, p.L), p.U);
+          o = fminf(fmaxf(fo[i], p.L), p.U);
           if (p.fallback) atomicAdd(p.fallback, 1ull);
         }
         out[(long long)yy * p.Wd] = o;
@@ -520,15 +532,15 @@ cudaError_t launch_t(const KParams& p, cudaStream_t s) {
   std::memset(&map, 0, sizeof(map));
   if ((p.Wd & 1) == 0 && !make_plane_map(&map, p, CC::NJ)) return cudaErrorInvalidValue;
   const long long ntr = (long long)((p.Wd + CR::WCOLS - 1) / CR::WCOLS) * ((p.in_rows + 3) / 4) * p.B;
-  const long long gr = std::min<long long>((ntr + kRowWarpsPerCta - 1) / kRowWarpsPerCta, (long long)occ_r * p.num_sms);
+  const long long gr = ntr;                // one warp task per CTA
   const long long ntc = (long long)((p.Wd + 31) / 32) * ((p.out_rows + CC::TROWS - 1) / CC::TROWS) * p.B;
-  const long long gc = std::min<long long>(ntc, (long long)occ_c * p.num_sms);
+  const long long gc = std::min<long long>(ntc, (long long)occ_c * p.num_sms);   // persistent, dynamic tasks
   if (p.ev[0]) cudaEventRecord(p.ev[0], s);
-  kr<<<(unsigned)gr, 32 * kRowWarpsPerCta, smem_r, s>>>(p);
+  kr<<<(unsigned)gr, 32 * kRowWarpsPerCta, smem_r, s>>>(p, p.counters);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (p.ev[1]) cudaEventRecord(p.ev[1], s);
-  kc<<<(unsigned)gc, 32 * (kColConsumers + 1), smem_c, s>>>(map, p);
+  kc<<<(unsigned)gc, 32 * (kColConsumers + 1), smem_c, s>>>(map, p, p.counters);
   e = cudaGetLastError();
   if (p.ev[2]) cudaEventRecord(p.ev[2], s);
   return e;

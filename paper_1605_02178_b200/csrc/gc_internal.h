@@ -39,6 +39,7 @@ struct KParams {
   long long seg_img_stride;   // elements between consecutive images in every segment
   float2* planes;         // row pass output [B][NP][in_rows][Wd] (plane pairs, row-major)
   int in_pitch;           // unused (reserved)
+  unsigned* counters;     // device scratch: dynamic task counters (zeroed on device)
   long long planes_img_stride; // float2 elements per image
   float* out;             // [B][out_rows][Wd]
   long long out_img_stride;

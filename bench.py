@@ -47,6 +47,7 @@ def _args():
     a.add_argument("--no-e2e", action="store_true")
     a.add_argument("--batch", type=int, default=None, help="override the batch size (profiling only)")
     a.add_argument("--no-cpu-baseline", action="store_true")
+    a.add_argument("--op", type=int, default=0, choices=[0, 1, 2], help="0 auto, 1 FIR, 2 O(1)")
     return a.parse_args()
 
 
@@ -59,14 +60,30 @@ def _dist():
 
 # ------------------------------------------------------------------ algorithmic work
 
-def flops_row(N, R, px):
-    """K_row per input pixel: eq. (7) row FIR 2(N+2)(2R+1) + planes (N+1 mul) + centring (6)."""
-    return px * (2 * (N + 2) * (2 * R + 1) + (N + 1) + 6)
+O1_FLOP_PER_PLANE = 50   # exact-window recursion per plane-sample and pass:
+#                          A, B (2 add) + box (2 add, 1 mul) + 5 resonators x (3 FMA + 1 add + 1 FMA)
 
 
-def flops_col(N, R, px):
-    """K_col per output pixel: eq. (7) column FIR 2(N+2)(2R+1) + eqs. (8)-(10) 6(N+1) + 8."""
-    return px * (2 * (N + 2) * (2 * R + 1) + 6 * (N + 1) + 8)
+def resolve_op(op, R):
+    """GC_OP_AUTO -> FIR for W_s <= 16, O(1) above (include/gc.h, gc_api.cpp)."""
+    return op if op in (1, 2) else (2 if R >= 17 else 1)
+
+
+def op_flop_per_plane(op, R):
+    """Algorithmic FLOP of eq. (7) per plane-pixel and pass: FIR 2(2R+1); O(1) 50."""
+    return 2 * (2 * R + 1) if op == 1 else O1_FLOP_PER_PLANE
+
+
+def flops_row(N, R, px, op=1):
+    """K_row per input pixel: eq. (7) along rows for N+2 planes + plane generation (N+1 mul,
+    once per sample for the FIR, for the entering and leaving samples for O(1)) + centring (6)."""
+    gen = (N + 1) + 6
+    return px * ((N + 2) * op_flop_per_plane(op, R) + (gen if op == 1 else 2 * gen))
+
+
+def flops_col(N, R, px, op=1):
+    """K_col per output pixel: eq. (7) along columns for N+2 planes + eqs. (8)-(10) 6(N+1) + 8."""
+    return px * ((N + 2) * op_flop_per_plane(op, R) + 6 * (N + 1) + 8)
 
 
 # ------------------------------------------------------------------ clocks during the timed region
@@ -221,9 +238,9 @@ def main():
 
     def step(events=None):
         if comm is not None:
-            gc.bilateral_band(x, cfg.H, row0, sigma_s, sigma_r, cfg.N, comm, out=out)
+            gc.bilateral_band(x, cfg.H, row0, sigma_s, sigma_r, cfg.N, comm, out=out, op=args.op)
         else:
-            gc.filter(x, sigma_s, sigma_r, cfg.N, out=out, events=events)
+            gc.filter(x, sigma_s, sigma_r, cfg.N, out=out, events=events, op=args.op)
 
     for _ in range(args.warmup):
         if flush is not None:
@@ -300,8 +317,9 @@ def main():
     roof = None
     kernels = None
     if row_ms is not None:
-        fr = flops_row(cfg.N, R, B * H * W)       # whole-image row pass (in_rows = H)
-        fc = flops_col(cfg.N, R, B * H * W)
+        op = resolve_op(args.op, R)
+        fr = flops_row(cfg.N, R, B * H * W, op)   # whole-image row pass (in_rows = H)
+        fc = flops_col(cfg.N, R, B * H * W, op)
         kernels = {"k_row": {"ms": row_ms, "tflops": fr / row_ms / 1e9},
                    "k_col": {"ms": col_ms, "tflops": fc / col_ms / 1e9}}
         dom = "k_col" if col_ms >= row_ms else "k_row"

@@ -58,8 +58,12 @@ typedef enum {
 /* Spatial operator used for eq. (7).  Both compute the truncated sum over Omega exactly
    as eq. (7) writes it (R3); they differ only in cost and rounding. */
 typedef enum {
-  GC_OP_AUTO = 0,  /* library choice by W_s                      */
-  GC_OP_FIR = 1    /* direct separable FIR, 2(2W_s+1) FMA per plane-pixel              */
+  GC_OP_AUTO = 0,  /* library choice by W_s: FIR for W_s <= 16, O1 above  */
+  GC_OP_FIR = 1,   /* direct separable FIR, 2(2W_s+1) FMA per plane-pixel; W_s <= 1024   */
+  GC_OP_O1 = 2     /* exact-window O(1) recursion: the truncated window of eq. (7) with
+                      the taps replaced by a 6-term cosine least-squares fit (max error
+                      ~1e-6 of the peak tap); 30 FMA-class ops per plane-pixel and pass,
+                      independent of sigma_s; W_s <= 4096                                  */
 } gc_operator;
 
 /* Human-readable name of a status code (static storage). */
@@ -136,6 +140,26 @@ gc_status gc_filter(const float* imgs, int B, int H, int W, const gc_params* p, 
  */
 gc_status gc_filter_host(const float* imgs_host, int B, int H, int W, const gc_params* p,
                          float* outs_host, void* stream);
+
+/*
+ * gc_gaussian — eq. (7) alone: the separable spatial Gaussian over the truncated
+ * window Omega = [-W_s, W_s]^2 with whole-sample symmetric extension, applied to B images
+ * [B][H][W] fp32 on the device (no centring, no clamping), with operator `op`.  This is the
+ * N+2-fold inner step of the GCF exposed on its own (operator tests, impulse responses).
+ * Errors: GC_EINVAL (sizes, sigma_s, op, null or overlapping pointers), GC_ERANGE (W_s above
+ * the operator's limit), GC_ECUDA.
+ */
+gc_status gc_gaussian(const float* imgs, int B, int H, int W, float sigma_s, int op, float* outs,
+                      void* stream);
+
+/*
+ * gc_operator_taps — host only, pure: the 1-D impulse response k[m], m = -W_s..W_s, that
+ * operator `op` applies along each axis at sigma_s (GC_OP_FIR: the normalised sampled taps of
+ * eq. 7; GC_OP_O1: the cosine expansion the O(1) kernels evaluate; GC_OP_AUTO: whichever
+ * gc_filter would pick).  taps_out: 2 W_s + 1 doubles (may be NULL to query W_s only);
+ * W_out (may be NULL) receives W_s.  Errors: GC_EINVAL, GC_ERANGE.
+ */
+gc_status gc_operator_taps(float sigma_s, int op, double* taps_out, int* W_out);
 
 /*
  * Row-band API (multi-GPU domain decomposition, one process per GPU).

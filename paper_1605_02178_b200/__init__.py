@@ -17,13 +17,13 @@ import numpy as np
 __all__ = [
     "GCError", "lib", "coeffs", "bilateral", "bilateral_batch", "bilateral_c", "filter",
     "filter_host", "filter_window", "band_plan", "Comm", "bilateral_band", "version",
-    "OP_AUTO", "OP_FIR",
+    "OP_AUTO", "OP_FIR", "OP_O1", "gaussian", "operator_taps",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgc.so")
 
-OP_AUTO, OP_FIR = 0, 1
+OP_AUTO, OP_FIR, OP_O1 = 0, 1, 2
 _STATUS = {0: "GC_OK", 1: "GC_EINVAL", 2: "GC_ERANGE", 3: "GC_ECUDA", 4: "GC_ENOMEM", 5: "GC_ENCCL"}
 
 
@@ -70,6 +70,8 @@ def _lib():
         L.gc_filter.argtypes = [vp, i, i, i, ctypes.POINTER(_Params), vp, vp]
         L.gc_filter_host.argtypes = [vp, i, i, i, ctypes.POINTER(_Params), vp, vp]
         L.gc_filter_window.argtypes = [ctypes.POINTER(vp), ip, ip, i, i, i, i, ctypes.POINTER(_Params), vp, vp]
+        L.gc_gaussian.argtypes = [vp, i, i, i, f, i, vp, vp]
+        L.gc_operator_taps.argtypes = [f, i, ctypes.POINTER(d), ip]
         L.gc_band_plan.argtypes = [i, i, i, ip, f, ip, ip, ip, ip, ip]
         L.gc_comm_unique_id.argtypes = [ctypes.c_char_p]
         L.gc_comm_init.argtypes = [i, i, ctypes.c_char_p, ctypes.POINTER(vp)]
@@ -77,7 +79,7 @@ def _lib():
         L.gc_bilateral_band.argtypes = [vp, i, i, i, i, ctypes.POINTER(_Params), vp, vp, vp]
         for name in ["gc_coeffs", "gc_bilateral", "gc_bilateral_batch", "gc_bilateral_c", "gc_filter",
                      "gc_filter_host", "gc_filter_window", "gc_band_plan", "gc_comm_unique_id",
-                     "gc_comm_init", "gc_comm_destroy", "gc_bilateral_band"]:
+                     "gc_comm_init", "gc_comm_destroy", "gc_bilateral_band", "gc_gaussian", "gc_operator_taps"]:
             getattr(L, name).restype = ctypes.c_int
         _LIB = L
     return _LIB
@@ -154,6 +156,30 @@ def filter(img, sigma_s, sigma_r, N, c=None, L=0.0, U=255.0, out=None, op=OP_AUT
     return out
 
 
+def gaussian(img, sigma_s, op=OP_AUTO, out=None, stream=None):
+    """gc_gaussian: eq. (7) alone on a [H, W] or [B, H, W] float32 CUDA tensor (operator `op`)."""
+    import torch
+    if img.dim() == 2:
+        B, (H, W) = 1, img.shape
+    elif img.dim() == 3:
+        B, H, W = img.shape
+    else:
+        raise ValueError("img must be [H, W] or [B, H, W]")
+    out = torch.empty_like(img) if out is None else out
+    _check(_lib().gc_gaussian(_dev_f32(img, "img"), B, H, W, float(sigma_s), int(op), _dev_f32(out, "out"),
+                              _stream(stream)), "gc_gaussian")
+    return out
+
+
+def operator_taps(sigma_s, op=OP_AUTO):
+    """gc_operator_taps (host only): the 1-D impulse response k[-W..W] operator `op` applies."""
+    Wr = ctypes.c_int()
+    _check(_lib().gc_operator_taps(float(sigma_s), int(op), None, ctypes.byref(Wr)), "gc_operator_taps")
+    t = (ctypes.c_double * (2 * Wr.value + 1))()
+    _check(_lib().gc_operator_taps(float(sigma_s), int(op), t, ctypes.byref(Wr)), "gc_operator_taps")
+    return np.array(t[:], dtype=np.float64)
+
+
 def bilateral(img, sigma_s, sigma_r, N, out=None, stream=None):
     """gc_bilateral: one [H, W] image, Chebyshev coefficients, [L, U] = [0, 255]."""
     import torch
@@ -200,7 +226,8 @@ def filter_host(img: np.ndarray, sigma_s, sigma_r, N, c=None, L=0.0, U=255.0, ou
     return out
 
 
-def filter_window(segs, H_global, out_row0, out_rows, sigma_s, sigma_r, N, c=None, out=None, stream=None):
+def filter_window(segs, H_global, out_row0, out_rows, sigma_s, sigma_r, N, c=None, out=None, stream=None,
+                  op=OP_AUTO):
     """gc_filter_window: segs = list of up to 3 (tensor [rows, W], global_row0)."""
     import torch
     if not 1 <= len(segs) <= 3:
@@ -214,7 +241,7 @@ def filter_window(segs, H_global, out_row0, out_rows, sigma_s, sigma_r, N, c=Non
         r0[k], nr[k] = int(g0), int(t.shape[0])
     if out is None:
         out = torch.empty((out_rows, W), dtype=torch.float32, device=segs[0][0].device)
-    p, keep = _params(N, sigma_s, sigma_r, c=c)
+    p, keep = _params(N, sigma_s, sigma_r, c=c, op=op)
     _check(_lib().gc_filter_window(ptrs, r0, nr, int(H_global), int(W), int(out_row0), int(out_rows),
                                    ctypes.byref(p), _dev_f32(out, "out"), _stream(stream)), "gc_filter_window")
     del keep
@@ -254,12 +281,13 @@ class Comm:
             self.handle = ctypes.c_void_p()
 
 
-def bilateral_band(band, H_global, row0, sigma_s, sigma_r, N, comm: Comm, c=None, out=None, stream=None):
+def bilateral_band(band, H_global, row0, sigma_s, sigma_r, N, comm: Comm, c=None, out=None, stream=None,
+                   op=OP_AUTO):
     """gc_bilateral_band: this rank's rows [row0, row0+H_band) of the GCF of a row-sharded image."""
     import torch
     H_band, W = band.shape
     out = torch.empty_like(band) if out is None else out
-    p, keep = _params(N, sigma_s, sigma_r, c=c)
+    p, keep = _params(N, sigma_s, sigma_r, c=c, op=op)
     _check(_lib().gc_bilateral_band(_dev_f32(band, "band"), H_band, W, int(H_global), int(row0), ctypes.byref(p),
                                     _dev_f32(out, "out"), comm.handle, _stream(stream)), "gc_bilateral_band")
     del keep

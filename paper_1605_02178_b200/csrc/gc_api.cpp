@@ -35,14 +35,46 @@ std::vector<double> taps_of(float sigma_s, int R) {
   return k;
 }
 
+// Constants of the O(1) exact-window operator (gc_o1.cu, gc_operator.cpp).
+void o1_constants(float sigma_s, KParams& k) {
+  const O1Fit& f = o1_fit_cached(sigma_s);
+  for (int q = 0; q < kO1K; q++) {
+    const double w = f.omega[q];
+    const double sh = std::sin(0.5 * w);
+    k.o1_alpha[q] = (float)f.alpha[q];
+    k.o1_nk[q] = (float)(-4.0 * sh * sh);
+    k.o1_a[q] = (float)std::cos(w * f.R);
+    k.o1_nb[q] = (float)(-std::cos(w * (f.R + 1)));
+  }
+}
+
+// Segment lengths of the O(1) passes: enough warps to fill the GPU (~16 per SM), segments no
+// shorter than 4 lead-ins (2W+1 samples each) unless the image itself is shorter.
+void o1_segments(KParams& k) {
+  const int target = k.num_sms * 16;
+  const int lead = 2 * k.R + 1;
+  auto split = [&](int len, long long base, int& seg, int& nseg) {
+    long long want = (target + base - 1) / base;
+    long long cap = std::max(1, len / (4 * lead));
+    int n = (int)std::max(1LL, std::min(want, cap));
+    seg = ((len + n - 1) / n + 31) / 32 * 32;
+    nseg = (len + seg - 1) / seg;
+  };
+  k.o1_groups = (k.NP + 3) / 4;
+  split(k.Wd, (long long)((k.in_rows + 31) / 32) * k.o1_groups * k.B, k.o1_seg_x, k.o1_nseg_x);
+  int G = 1;
+  while ((k.NP + G - 1) / G > (G == 8 ? 5 : 4) && G < 8) G *= 2;
+  split(k.out_rows, (long long)((k.Wd + 32 / G - 1) / (32 / G)) * k.B, k.o1_seg_y, k.o1_nseg_y);
+}
+
 gc_status validate_params(const gc_params* p) {
   if (!p) return GC_EINVAL;
   if (p->N < 0) return GC_EINVAL;
   if (p->N > GC_N_MAX) return GC_ERANGE;
   if (!finite_pos(p->sigma_s) || !finite_pos(p->sigma_r)) return GC_EINVAL;
   if (!std::isfinite(p->L) || !std::isfinite(p->U) || !(p->U > p->L)) return GC_EINVAL;
-  if (p->op != GC_OP_AUTO && p->op != GC_OP_FIR) return GC_EINVAL;
-  if (radius_of(p->sigma_s) > kMaxFirW) return GC_ERANGE;
+  if (p->op != GC_OP_AUTO && p->op != GC_OP_FIR && p->op != GC_OP_O1) return GC_EINVAL;
+  if (radius_of(p->sigma_s) > (p->op == GC_OP_FIR ? kMaxFirW : kO1MaxW)) return GC_ERANGE;
   if (p->c) {
     for (int n = 0; n <= p->N; n++)
       if (!std::isfinite(p->c[n])) return GC_EINVAL;
@@ -90,6 +122,10 @@ gc_status fill_constants(const gc_params* p, KParams& k, std::vector<float2>& ta
   k.ex_k = (float)(-0.5 * mu * 1.4426950408889634);
   k.fallback = p->fallback_count;
   for (int i = 0; i < 3; i++) k.ev[i] = reinterpret_cast<cudaEvent_t>(p->events[i]);
+  // operator: GC_OP_AUTO = FIR for small radii (fewer instructions), O(1) above
+  const int op = p->op == GC_OP_AUTO ? (k.R >= kO1AutoMinW ? GC_OP_O1 : GC_OP_FIR) : p->op;
+  k.op = op;
+  if (op == GC_OP_O1) o1_constants(p->sigma_s, k);
   return GC_OK;
 }
 
@@ -123,7 +159,8 @@ gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) 
   cudaGetDevice(&dev);
   k.num_sms = 148;
   cudaDeviceGetAttribute(&k.num_sms, cudaDevAttrMultiProcessorCount, dev);
-  k.in_pitch = k.in_rows;
+  const int op = k.op;
+  if (op == GC_OP_O1) o1_segments(k);
   const size_t plane_elems = (size_t)k.NP * k.in_rows * k.Wd;
   float2* planes = nullptr;
   float2* taps_dev = nullptr;
@@ -131,7 +168,7 @@ gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) 
   cudaError_t e = cudaMallocAsync((void**)&planes, plane_elems * k.B * sizeof(float2) + 256, s);
   if (e != cudaSuccess) return cuda_status(e);
   k.counters = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(planes) + plane_elems * k.B * sizeof(float2));
-  if (k.R > kMaxTemplW) {
+  if (op == GC_OP_FIR && k.R > kMaxTemplW) {
     e = cudaMallocAsync((void**)&taps_dev, taps_host.size() * sizeof(float2), s);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(taps_dev, taps_host.data(), taps_host.size() * sizeof(float2),
@@ -145,7 +182,7 @@ gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) 
   k.planes = planes;
   k.planes_img_stride = (long long)plane_elems;
   k.taps_g = taps_dev;
-  e = launch_fir_two_pass(k, s);
+  e = op == GC_OP_O1 ? launch_o1_two_pass(k, s) : launch_fir_two_pass(k, s);
   cudaError_t e2 = cudaFreeAsync(planes, s);
   if (taps_dev) cudaFreeAsync(taps_dev, s);
   if (e != cudaSuccess) return cuda_status(e);
@@ -265,6 +302,59 @@ gc_status gc_filter(const float* imgs, int B, int H, int W, const gc_params* p, 
   k.out = outs;
   k.out_img_stride = (long long)H * W;
   return run(k, taps_host, reinterpret_cast<cudaStream_t>(stream));
+}
+
+gc_status gc_gaussian(const float* imgs, int B, int H, int W, float sigma_s, int op, float* outs, void* stream) {
+  gc_params p;
+  gc_params_init(&p, 0, sigma_s, 1000.f);   // N = 0, one plane pair (f, 0); sigma_r unused
+  p.op = op;
+  gc_status st = validate_params(&p);
+  if (st != GC_OK) return st;
+  if (!imgs || !outs || B < 1 || H < 1 || W < 1) return GC_EINVAL;
+  const size_t bytes = (size_t)B * H * W * sizeof(float);
+  if (overlap(imgs, bytes, outs, bytes)) return GC_EINVAL;
+  KParams k;
+  std::memset(&k, 0, sizeof(k));
+  std::vector<float2> taps_host;
+  st = fill_constants(&p, k, taps_host);
+  if (st != GC_OK) return st;
+  k.raw = 1;
+  k.H = H;
+  k.Wd = W;
+  k.B = B;
+  k.in_row0 = 0;
+  k.in_rows = H;
+  k.out_row0 = 0;
+  k.out_rows = H;
+  k.seg[0] = Seg{imgs, 0, H};
+  k.seg[1] = Seg{imgs, -1, 0};
+  k.seg[2] = Seg{imgs, -1, 0};
+  k.seg_img_stride = (long long)H * W;
+  k.out = outs;
+  k.out_img_stride = (long long)H * W;
+  return run(k, taps_host, reinterpret_cast<cudaStream_t>(stream));
+}
+
+gc_status gc_operator_taps(float sigma_s, int op, double* taps_out, int* W_out) {
+  if (!std::isfinite(sigma_s) || !(sigma_s > 0)) return GC_EINVAL;
+  if (op != GC_OP_AUTO && op != GC_OP_FIR && op != GC_OP_O1) return GC_EINVAL;
+  const int R = radius_of(sigma_s);
+  if (R > (op == GC_OP_FIR ? kMaxFirW : kO1MaxW)) return GC_ERANGE;
+  if (op == GC_OP_AUTO) op = R >= kO1AutoMinW ? GC_OP_O1 : GC_OP_FIR;
+  if (W_out) *W_out = R;
+  if (!taps_out) return GC_OK;
+  if (op == GC_OP_FIR) {
+    const std::vector<double> t = taps_of(sigma_s, R);
+    std::copy(t.begin(), t.end(), taps_out);
+  } else {
+    const O1Fit& f = o1_fit_cached(sigma_s);
+    for (int m = -R; m <= R; m++) {
+      double v = 0;
+      for (int q = 0; q < kO1K; q++) v += f.alpha[q] * std::cos(f.omega[q] * m);
+      taps_out[m + R] = v;
+    }
+  }
+  return GC_OK;
 }
 
 gc_status gc_bilateral(const float* img, int H, int W, float sigma_s, float sigma_r, int N, float* out,

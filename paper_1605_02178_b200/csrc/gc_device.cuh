@@ -29,6 +29,26 @@ __device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
   return d;
 }
 
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  float2 d;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&d))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+  return d;
+}
+
+__device__ __forceinline__ float2 f2sub(float2 a, float2 b) {
+  float2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&d))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+  return d;
+}
+
+__device__ __forceinline__ float2 f2s(float s) { return make_float2(s, s); }
+
 // Whole-sample symmetric extension (R5): period 2n-2, n = 1 -> 0.
 __device__ __forceinline__ int mirror(int p, int n) {
   if (n <= 1) return 0;

@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(32 * kRowWarpsPerCta, 16) k_row_t(const KParam
       if (c < C::SW) {
         float a, e;
         centre(p, fv[rr][k], a, e);
+        if (p.raw) { e = fv[rr][k]; a = 0.f; }                      // gc_gaussian: (f, 0)
         sPsi[rr * C::SWP + C::pad(c)] = make_float2(e, e * a);      // pair 0: e (1, a')
         sA2[rr * C::A2W + c] = a * a;
       }
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 3)
 
   // ------------------------------------------------ consumer warps
   const int seg = warp;
-  float fo[RY], av[RY], P[RY], Q[RY], vpy[RY], pwx[RY];
+  float fo[RY], av[RY], P[RY], Q[RY], vpy[RY], pwx[RY], raw0[RY];
   int b = 0, x = 0, y0 = 0;
   for (int k = 0;; k++) {
     const int s = k % kColStages;
@@ -364,6 +365,7 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 3)
     if (pp == 0) {
 #pragma unroll
       for (int i = 0; i < RY; i++) {
+        raw0[i] = acc[i].x;
         float a, e;
         centre(p, fo[i], a, e);
         av[i] = a;
@@ -394,7 +396,9 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 3)
         if (yy > last) break;
         const float Qi = Q[i], Pi = P[i];
         float o;
-        if (Qi > 0.f && isfinite(Qi) && isfinite(Pi)) {
+        if (p.raw) {
+          o = raw0[i];
+        } else if (Qi > 0.f && isfinite(Qi) && isfinite(Pi)) {
           o = p.t_c + p.t_h * (Pi / Qi);                 // eq. (10) + uncentring
         } else {                                          // guard (R8)
           o = fminf(fmaxf(fo[i], p.L), p.U);
@@ -424,7 +428,9 @@ __global__ void __launch_bounds__(256) k_row_rt(const KParams p) {
     const float* src = row_ptr(p, b, p.in_row0 + rr);
     for (int c = tid; c < SW; c += 256) {
       float a, e;
-      centre(p, __ldg(src + mirror(x0 - R + c, p.Wd)), a, e);
+      const float fv = __ldg(src + mirror(x0 - R + c, p.Wd));
+      centre(p, fv, a, e);
+      if (p.raw) { e = fv; a = 0.f; }
       sPL[r * SW + c] = make_float2(e, e * a);
       sA2[r * SW + c] = make_float2(a * a, a * a);
     }
@@ -459,7 +465,7 @@ __global__ void __launch_bounds__(256) k_col_rt(const KParams p) {
   centre(p, f, a, e);
   const float a2 = a * a;
   float2 pw = make_float2(1.f, a), P2 = make_float2(0.f, 0.f), Q2 = make_float2(0.f, 0.f);
-  float vpy = 0.f;
+  float vpy = 0.f, raw0 = 0.f;
   const long long pstride = (long long)p.in_rows * p.Wd;
   for (int pp = 0; pp < p.NP; pp++) {
     const float2* pl = p.planes + b * p.planes_img_stride + pp * pstride + x;
@@ -468,6 +474,7 @@ __global__ void __launch_bounds__(256) k_col_rt(const KParams p) {
       const int q = mirror(gy + m - R, p.H) - p.in_row0;
       acc = f2fma(p.taps_g[m], __ldg(pl + (long long)q * p.Wd), acc);
     }
+    if (pp == 0) raw0 = acc.x;
     const float2 v2 = f2mul(p.chat2[pp], pw);
     Q2 = f2fma(v2, acc, Q2);
     P2 = f2fma(make_float2(vpy, v2.x), acc, P2);
@@ -476,7 +483,9 @@ __global__ void __launch_bounds__(256) k_col_rt(const KParams p) {
   }
   const float Q = Q2.x + Q2.y, P = P2.x + P2.y;
   float o;
-  if (Q > 0.f && isfinite(Q) && isfinite(P)) {
+  if (p.raw) {
+    o = raw0;
+  } else if (Q > 0.f && isfinite(Q) && isfinite(P)) {
     o = p.t_c + p.t_h * (P / Q);
   } else {
     o = fminf(fmaxf(f, p.L), p.U);

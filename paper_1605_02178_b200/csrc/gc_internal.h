@@ -18,6 +18,9 @@ constexpr int kMaxPlanes = GC_N_MAX + 2 + 1;   // N+2 planes, rounded up to even
 constexpr int kMaxPairs = (kMaxPlanes + 1) / 2;
 constexpr int kMaxTemplW = 24;                 // FIR radius range with unrolled kernels
 constexpr int kMaxFirW = 1024;                 // runtime-W FIR kernels (taps in global)
+constexpr int kO1K = 6;                        // O(1) operator: cosine terms (q = 0 is the box)
+constexpr int kO1MaxW = 4096;                  // O(1) operator radius limit
+constexpr int kO1AutoMinW = 17;                // GC_OP_AUTO: FIR for W <= 16, O(1) above
 
 // One input-row segment (device pointer to rows [row0, row0+rows) of the global image).
 struct Seg {
@@ -38,7 +41,7 @@ struct KParams {
   Seg seg[3];             // input rows (see gc_filter_window)
   long long seg_img_stride;   // elements between consecutive images in every segment
   float2* planes;         // row pass output [B][NP][in_rows][Wd] (plane pairs, row-major)
-  int in_pitch;           // unused (reserved)
+  int op;                 // resolved operator: GC_OP_FIR or GC_OP_O1 (host side)
   unsigned* counters;     // device scratch: dynamic task counters (zeroed on device)
   long long planes_img_stride; // float2 elements per image
   float* out;             // [B][out_rows][Wd]
@@ -55,10 +58,34 @@ struct KParams {
   float tap[2 * kMaxTemplW + 1];   // k_m, m = 0..2R (unrolled kernels; FFMA2 scalar broadcast)
   int ctas_per_sm;                 // persistent-grid sizing (host side)
   int num_sms;
+  // O(1) exact-window operator (gc_o1.cu): k_m ~ sum_q alpha_q cos(w_q m) on |m| <= W
+  float o1_alpha[kO1K];            // alpha_q (q = 0: box term)
+  float o1_nk[kO1K];               // -4 sin^2(w_q / 2)   (Reinsch form of the resonator)
+  float o1_a[kO1K];                // cos(w_q W)
+  float o1_nb[kO1K];               // -cos(w_q (W + 1))
+  int o1_seg_x, o1_nseg_x;         // row pass: x-segment length (multiple of 32) and count
+  int o1_seg_y, o1_nseg_y;         // column pass: y-segment length and count
+  int o1_groups;                   // row pass: plane-pair groups (<= 4 pairs each)
+  int raw;                         // 1: eq. (7) of f itself (gc_gaussian): pair 0 = (f, 0), out = Fbar_0
 };
+
+// O(1) operator constants for radius R = ceil(3 sigma_s) (gc_api.cpp): least-squares K-term
+// cosine expansion of the truncated taps on |m| <= R, half-period Lh searched for the smallest
+// max error.  alpha/omega in binary64; fit_err = max_m |expansion - k_m|.
+struct O1Fit {
+  int R;
+  double Lh;
+  double alpha[kO1K];
+  double omega[kO1K];
+  double fit_err;
+};
+const O1Fit& o1_fit_cached(float sigma_s);
 
 // Launch the two-pass FIR pipeline (row pass + column pass with recombination) on
 // `stream`.  Scratch (the plane buffer) must already be in p.planes.
 cudaError_t launch_fir_two_pass(const KParams& p, cudaStream_t stream);
+
+// Launch the two-pass O(1) exact-window pipeline (gc_o1.cu).  Same buffers and semantics.
+cudaError_t launch_o1_two_pass(const KParams& p, cudaStream_t stream);
 
 }  // namespace gc

@@ -92,7 +92,10 @@ def test_device_entry_points_validate_before_cuda(gc):
     assert lib.gc_bilateral_c(fake, 8, 8, 3.0, 30.0, 5, None, fake2, None) == 1
     cc = (ctypes.c_double * 6)(1, 1, 0.5, float("inf"), 0, 0)
     assert lib.gc_bilateral_c(fake, 8, 8, 3.0, 30.0, 5, cc, fake2, None) == 1
-    assert lib.gc_bilateral(fake, 8, 8, 1000.0, 30.0, 5, fake2, None) == 2      # W_s > kMaxFirW
+    assert lib.gc_bilateral(fake, 8, 8, 2000.0, 30.0, 5, fake2, None) == 2      # W_s > O(1) limit
+    assert lib.gc_gaussian(fake, 1, 8, 8, 2.0, 7, fake2, None) == 1               # unknown operator
+    assert lib.gc_gaussian(fake, 1, 8, 8, 500.0, 1, fake2, None) == 2             # W_s > FIR limit
+    assert lib.gc_gaussian(fake, 1, 8, 8, 2.0, 1, fake, None) == 1                # aliased
 
 
 def test_status_strings(gc):
@@ -123,3 +126,21 @@ def test_band_plan_errors(gc):
         gc.band_plan(100, 0, 2, [92, 8], 3.0)             # band <= W_s = 9
     with pytest.raises(gc.GCError):
         gc.band_plan(100, 2, 2, [50, 50], 3.0)            # rank out of range
+
+
+@pytest.mark.parametrize("sigma_s", [0.3, 1.0, 2.0, 3.0, 4.0, 5.0, 7.5, 10.0, 16.0, 20.0, 40.0, 100.0, 400.0])
+def test_operator_taps(gc, sigma_s):
+    """gc_operator_taps: FIR = the sampled, truncated, normalised taps of eq. (7) (oracle
+    spatial_taps); the O(1) operator's cosine expansion is within 1e-6 of the peak tap
+    on the same window and sums to 1 (a constant plane is preserved)."""
+    k, W = oracle.spatial_taps(float(np.float32(sigma_s)))     # the ABI takes sigma_s as fp32
+    fir = gc.operator_taps(sigma_s, gc.OP_FIR) if W <= 1024 else None
+    o1 = gc.operator_taps(sigma_s, gc.OP_O1)
+    assert len(o1) == 2 * W + 1
+    if fir is not None:
+        assert np.max(np.abs(fir - k)) <= 1e-15
+    assert np.max(np.abs(o1 - k)) <= 1e-6 * k.max()
+    assert abs(o1.sum() - 1.0) <= 1e-5
+    assert np.allclose(o1, o1[::-1], rtol=0, atol=1e-15)            # symmetric (cosines)
+    auto = gc.operator_taps(sigma_s, gc.OP_AUTO)
+    assert np.array_equal(auto, o1 if W >= 17 else fir)

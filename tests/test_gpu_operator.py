@@ -1,0 +1,118 @@
+"""GPU tests of the spatial operator of eq. (7) on its own (gc_gaussian) and of
+the GCF with the O(1) exact-window operator (GC_OP_O1) against the fp64 oracle.
+
+The oracle's eq. (7) is the separable truncated FIR (oracle.gauss_fir); the O(1) operator
+evaluates the same window with a 6-term cosine fit of the taps (max error 1e-6 of the
+peak tap, pinned in test_abi.py::test_operator_taps) and fp32 recursions."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from synth import CONFIGS, config_image
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS, RMS = 1e-2, 1e-3
+OP_FIR, OP_O1 = 1, 2
+
+
+@pytest.fixture(scope="module")
+def gc(cuda_device):
+    import paper_1605_02178_b200 as gc
+    return gc
+
+
+def _gauss(gc, img, sigma_s, op):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(img, dtype=np.float32)).cuda()
+    out = gc.gaussian(t, sigma_s, op=op)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("op", [OP_FIR, OP_O1])
+@pytest.mark.parametrize("sigma_s", [2.0, 5.0, 16.0])
+def test_impulse_response(gc, op, sigma_s):
+    """A unit impulse far from the edges returns the outer product of the 1-D taps."""
+    W = math.ceil(3 * sigma_s)
+    n = 2 * W + 41
+    img = np.zeros((n, n + 7), np.float32)
+    cy, cx = n // 2, (n + 7) // 2
+    img[cy, cx] = 1.0
+    out = _gauss(gc, img, sigma_s, op)
+    k = gc.operator_taps(sigma_s, op)
+    ref = np.zeros_like(out)
+    ref[cy - W:cy + W + 1, cx - W:cx + W + 1] = np.outer(k, k)
+    assert np.max(np.abs(out - ref)) <= 2e-7 * k.max() ** 2 * 10 + 1e-9
+    kx, _ = oracle.spatial_taps(sigma_s)
+    ref2 = np.zeros_like(out)
+    ref2[cy - W:cy + W + 1, cx - W:cx + W + 1] = np.outer(kx, kx)
+    assert np.max(np.abs(out - ref2)) <= 3e-6 * kx.max() ** 2
+
+
+@pytest.mark.parametrize("op", [OP_FIR, OP_O1])
+@pytest.mark.parametrize("sigma_s,H,W", [(1.0, 33, 47), (3.0, 256, 256), (5.0, 131, 300), (10.0, 200, 77),
+                                         (16.0, 300, 290), (40.0, 130, 170), (3.0, 1, 50), (4.0, 37, 1),
+                                         (12.0, 5, 9)])
+def test_gaussian_vs_oracle(gc, op, sigma_s, H, W):
+    """eq. (7) of a config-like 0-255 image: GPU vs oracle.gauss_fir (separable fp64 FIR
+    with whole-sample mirroring, repeated when W_s >= n)."""
+    if op == OP_FIR and math.ceil(3 * sigma_s) > 1024:
+        pytest.skip("FIR radius limit")
+    img = config_image("c2", H=max(H, 2), W=max(W, 2))[:H, :W]
+    out = _gauss(gc, img, sigma_s, op)
+    ref = oracle.gauss_fir(img.astype(np.float64), sigma_s)
+    tol = 2e-4 if op == OP_FIR else 2e-3
+    assert np.max(np.abs(out - ref)) <= tol
+
+
+@pytest.mark.parametrize("cfg,sigma_s,H,W", [
+    ("c1", 3.0, 256, 256),
+    ("c2", 5.0, 1024, 1024),
+    ("c2", 5.0, 150, 131),
+    ("c3", 2.0, 300, 517),
+    ("c3", 10.0, 200, 333),
+    ("c3", 20.0, 190, 210),
+    ("c3", 40.0, 130, 170),
+    ("c3", 40.0, 700, 650),
+    ("c4", 4.0, 129, 1024),
+    ("c5", 16.0, 300, 290),
+    ("c5", 16.0, 1030, 1100),
+])
+def test_parity_twin_o1(gc, cfg, sigma_s, H, W):
+    """GCF with the O(1) operator vs the oracle at the sigma_r twins (R1)."""
+    import torch
+    c = CONFIGS[cfg]
+    img = config_image(c, H=H, W=W)
+    t = torch.from_numpy(img).cuda()
+    out = gc.filter(t, sigma_s, c.sigma_r_twin, c.N, op=OP_O1)
+    torch.cuda.synchronize()
+    out = out.cpu().numpy().astype(np.float64)
+    ref, nfb = oracle.gc_filter(img, sigma_s, c.sigma_r_twin, c.N)
+    assert nfb == 0
+    err = np.abs(out - ref)
+    ma, rms = float(err.max()), float(math.sqrt(np.mean(err ** 2)))
+    assert ma <= MAX_ABS and rms <= RMS, f"{cfg} sigma_s={sigma_s} {H}x{W}: max-abs {ma:.3e} rms {rms:.3e}"
+
+
+def test_o1_and_fir_agree_on_paper_regime(gc):
+    """sigma_r = 30, N = 28 (Table II's operating point): both operators vs the oracle."""
+    import torch
+    img = config_image("c2", H=160, W=170)
+    t = torch.from_numpy(img).cuda()
+    ref, _ = oracle.gc_filter(img, 5.0, 30.0, 28)
+    for op in [OP_FIR, OP_O1]:
+        out = gc.filter(t, 5.0, 30.0, 28, op=op).cpu().numpy().astype(np.float64)
+        assert np.max(np.abs(out - ref)) <= MAX_ABS, op
+
+
+def test_o1_large_degree(gc):
+    """N = 40 (21 plane pairs: 4 lanes per column in the O(1) column pass)."""
+    import torch
+    img = config_image("c2", H=90, W=100)
+    t = torch.from_numpy(img).cuda()
+    ref, _ = oracle.gc_filter(img, 6.0, 30.0, 40)
+    out = gc.filter(t, 6.0, 30.0, 40, op=OP_O1).cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(out - ref)) <= MAX_ABS

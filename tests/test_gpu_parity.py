@@ -170,14 +170,16 @@ def test_deterministic(gc):
     assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("sigma_s", [3.0, 16.0])
-def test_virtual_bands_equal_whole_image(gc, sigma_s):
+@pytest.mark.parametrize("sigma_s,op", [(3.0, 1), (16.0, 1), (16.0, 2), (6.0, 2)])
+def test_virtual_bands_equal_whole_image(gc, sigma_s, op):
     """Single-GPU emulation of the row-band path: each band filtered by gc_filter_window
-    from three segments (top halo, band, bottom halo) equals the whole-image result."""
+    from three segments (top halo, band, bottom halo) equals the whole-image result —
+    bit for bit with the FIR operator; to rounding with the O(1) operator, whose line
+    segments (and so its fp32 summation order) depend on the window's extent."""
     import torch
     img = config_image("c5", H=400, W=333)
     t = torch.from_numpy(img).cuda()
-    whole = gc.filter(t, sigma_s, 55.0, 12)
+    whole = gc.filter(t, sigma_s, 55.0, 12, op=op)
     R = math.ceil(3 * sigma_s)
     bands = [0, 130, 260, 400]
     for k in range(3):
@@ -188,9 +190,12 @@ def test_virtual_bands_equal_whole_image(gc, sigma_s):
         segs.append((t[r0:r1].clone(), r0))
         if k < 2:
             segs.append((t[r1:r1 + R].clone(), r1))
-        part = gc.filter_window(segs, 400, r0, r1 - r0, sigma_s, 55.0, 12)
+        part = gc.filter_window(segs, 400, r0, r1 - r0, sigma_s, 55.0, 12, op=op)
         torch.cuda.synchronize()
-        assert torch.equal(part, whole[r0:r1]), k
+        if op == 1:
+            assert torch.equal(part, whole[r0:r1]), k
+        else:
+            assert float((part - whole[r0:r1]).abs().max()) <= 1e-3, k
 
 
 def test_window_rejects_missing_rows(gc):

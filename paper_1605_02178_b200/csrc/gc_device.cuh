@@ -50,12 +50,23 @@ __device__ __forceinline__ float2 f2sub(float2 a, float2 b) {
 __device__ __forceinline__ float2 f2s(float s) { return make_float2(s, s); }
 
 // Whole-sample symmetric extension (R5): period 2n-2, n = 1 -> 0.
-__device__ __forceinline__ int mirror(int p, int n) {
+static __device__ __noinline__ int mirror_slow(int p, int n) {
   if (n <= 1) return 0;
   const int period = 2 * n - 2;
   p = p < 0 ? -p : p;
   p %= period;
   return p < n ? p : period - p;
+}
+__device__ __forceinline__ int mirror(int p, int n) {
+  return (unsigned)p < (unsigned)n ? p : mirror_slow(p, n);   // interior: no arithmetic
+}
+
+// 2^x on the MUFU (one instruction; denormal results flush to 0, which only occurs for
+// e = exp(-g^2/2sr^2) < 2^-126, i.e. terms far below fp32 resolution of the sums).
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 // Pointer to global row gy of image b, found in the input segments.
@@ -73,7 +84,13 @@ __device__ __forceinline__ const float* row_ptr(const KParams& p, int b, int gy)
 __device__ __forceinline__ void centre(const KParams& p, float f, float& a, float& e) {
   f = fminf(fmaxf(f, p.L), p.U);            // inputs clamped to [L, U] (R7)
   a = (f - p.t_c) * p.inv_th;
-  e = exp2f(p.ex_k * (a * a));
+  e = ex2_ftz(p.ex_k * (a * a));
+}
+
+// a' alone (the recombination of eqs. (8)-(9) needs no Gaussian factor).
+__device__ __forceinline__ float centre_a(const KParams& p, float f) {
+  f = fminf(fmaxf(f, p.L), p.U);
+  return (f - p.t_c) * p.inv_th;
 }
 
 }  // namespace gc

@@ -38,121 +38,180 @@
 namespace gc {
 
 constexpr int kO1Warps = 4;     // warps per CTA (independent tasks)
-constexpr int kO1CH = 32;       // f positions per staged chunk
-constexpr int kO1OC = 16;       // output positions per store chunk
+constexpr int kO1CH = 16;       // positions per staged chunk
+constexpr int kO1TS = 17;       // staged tile row stride (float2): 2 wavefronts per warp access
+constexpr int kO1OC = 8;        // output positions per store chunk (= main-loop unroll)
 constexpr int kO1RowNPG = 4;    // plane pairs per row-pass warp (max)
+constexpr int kO1OS = 36;       // out tile position stride (float2): 2 wavefronts per access
 
 struct RowO1Smem {
-  float fin[kO1CH][33];                  // entering stream  [pos][row]
-  float fout[kO1CH][33];                 // leaving stream   [pos][row]
-  float2 o[kO1RowNPG][kO1OC][33];        // filtered pairs   [pair][pos][row] (word stride 66)
+  float2 fin[32 * kO1TS];                  // entering stream  [row][pos] = (e a'^{2p0}, a')
+  float2 fout[32 * kO1TS];                 // leaving stream   [row][pos]
+  float2 o[kO1RowNPG][kO1OC][kO1OS];       // filtered pairs   [pair][pos][row]
 };
 
-// Stage f at positions pb .. pb+31 (mirrored in x) of rows r0 .. r0+31 into t[pos][row].
-__device__ __forceinline__ void o1_stage_f(const KParams& p, float (*t)[33], int b, int r0, int pb, int lane) {
-  const int gx = mirror(pb + lane, p.Wd);
-  float v[32];
+// Stage this lane's row at the 16 positions of the aligned chunk [pc, pc+16) (whole-sample
+// mirroring in x) as v = (F'_{2p0}, a') = (e a'^{2p0}, a') of eq. (6), or (f, 0) for
+// gc_gaussian; then F'_{2p0+1} = v.x v.y and the pair step is a'^2 = v.y^2.
+__device__ __forceinline__ void o1_stage_row(const KParams& p, float2* t, const float* rowp, int pc, int lane,
+                                            bool vec, int p0) {
+  float v[kO1CH];
+  if (vec && pc >= 0 && pc + kO1CH <= p.Wd) {
 #pragma unroll
-  for (int k = 0; k < 32; k++) {
-    const int y = min(r0 + k, p.in_rows - 1);
-    v[k] = __ldg(row_ptr(p, b, p.in_row0 + y) + gx);
+    for (int k = 0; k < kO1CH / 4; k++) {
+      const float4 u = __ldg(reinterpret_cast<const float4*>(rowp + pc) + k);
+      v[4 * k] = u.x; v[4 * k + 1] = u.y; v[4 * k + 2] = u.z; v[4 * k + 3] = u.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kO1CH; k++) v[k] = __ldg(rowp + mirror(pc + k, p.Wd));
   }
+  float2* d = t + lane * kO1TS;
   __syncwarp();
+  if (p.raw) {
 #pragma unroll
-  for (int k = 0; k < 32; k++) t[lane][k] = v[k];
+    for (int k = 0; k < kO1CH; k++) d[k] = make_float2(v[k], 0.f);
+  } else if (p0 == 0) {
+#pragma unroll
+    for (int k = 0; k < kO1CH; k++) {
+      float a, e;
+      centre(p, v[k], a, e);
+      d[k] = make_float2(e, a);
+    }
+  } else if (p0 == 4) {
+#pragma unroll
+    for (int k = 0; k < kO1CH; k++) {
+      float a, e;
+      centre(p, v[k], a, e);
+      const float a2 = a * a, a4 = a2 * a2;
+      d[k] = make_float2(e * (a4 * a4), a);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kO1CH; k++) {
+      float a, e;
+      centre(p, v[k], a, e);
+      float pw = 1.f, base = a * a;
+      for (int kk = p0; kk; kk >>= 1) {
+        if (kk & 1) pw *= base;
+        base *= base;
+      }
+      d[k] = make_float2(e * pw, a);
+    }
+  }
   __syncwarp();
 }
 
-// psi for the first pair of the group: (F'_{2p0}, F'_{2p0+1}) = e a'^{2p0} (1, a'), and a'^2.
-__device__ __forceinline__ float2 o1_psi0(const KParams& p, float f, int p0, float& a2) {
-  if (p.raw) {
-    a2 = 0.f;
-    return make_float2(f, 0.f);
+// One step of the exact-window recursion for one plane pair (Reinsch form).
+//   A = x(i+W+1) + x(i-W-1), B = x(i+W) + x(i-W), box: S0 += x(i+W+1) - x(i-W)
+__device__ __forceinline__ void o1_update(const KParams& p, float2& S0, float2* S, float2* D, float2 A, float2 B,
+                                          float2 xin, float2 xout) {
+  S0 = f2add(S0, f2sub(xin, xout));
+#pragma unroll
+  for (int t = 0; t < kO1K - 1; t++) {
+    float2 d = f2fma(f2s(p.o1_nk[t + 1]), S[t], D[t]);
+    d = f2fma(f2s(p.o1_a[t + 1]), A, d);
+    d = f2fma(f2s(p.o1_nb[t + 1]), B, d);
+    D[t] = d;
+    S[t] = f2add(S[t], d);
   }
-  float a, e;
-  centre(p, f, a, e);
-  a2 = a * a;
-  float pw = 1.f, base = a2;
-  for (int k = p0; k; k >>= 1) {   // a'^{2 p0} by binary powering (p0 warp-uniform)
-    if (k & 1) pw *= base;
-    base *= base;
+}
+
+__device__ __forceinline__ float2 o1_output(const KParams& p, float2 S0, const float2* S) {
+  float2 y = f2mul(f2s(p.o1_alpha[0]), S0);
+#pragma unroll
+  for (int t = 0; t < kO1K - 1; t++) y = f2fma(f2s(p.o1_alpha[t + 1]), S[t], y);
+  return y;
+}
+
+template <int NPG>
+struct RowO1State {
+  float2 S0[NPG], S[NPG][kO1K - 1], D[NPG][kO1K - 1], Ep[NPG], Lp[NPG];
+};
+
+// One output step at x (window centred on x), output slot j of the current store chunk.
+template <int NPG>
+__device__ __forceinline__ void row_o1_step(const KParams& p, RowO1Smem& sm, RowO1State<NPG>& st, int x, int j,
+                                            const float* rowp, bool vec, int p0, int lane) {
+  const int R = p.R;
+  const int pe_pos = x + R + 1, pl_pos = x - R;
+  if ((pe_pos & (kO1CH - 1)) == 0) o1_stage_row(p, sm.fin, rowp, pe_pos, lane, vec, p0);
+  if ((pl_pos & (kO1CH - 1)) == 0) o1_stage_row(p, sm.fout, rowp, pl_pos, lane, vec, p0);
+  const float2 ve = sm.fin[lane * kO1TS + (pe_pos & (kO1CH - 1))];
+  const float2 vl = sm.fout[lane * kO1TS + (pl_pos & (kO1CH - 1))];
+  float2 pe = make_float2(ve.x, ve.x * ve.y), pl = make_float2(vl.x, vl.x * vl.y);
+  const float a2e = ve.y * ve.y, a2l = vl.y * vl.y;
+#pragma unroll
+  for (int q = 0; q < NPG; q++) {
+    sm.o[q][j][lane] = o1_output(p, st.S0[q], st.S[q]);
+    o1_update(p, st.S0[q], st.S[q], st.D[q], f2add(pe, st.Lp[q]), f2add(st.Ep[q], pl), pe, pl);
+    st.Ep[q] = pe;
+    st.Lp[q] = pl;
+    pe = f2mul(pe, f2s(a2e));
+    pl = f2mul(pl, f2s(a2l));
   }
-  const float ep = e * pw;
-  return make_float2(ep, ep * a);
 }
 
 template <int NPG>
 __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int b, int r0, int xs, int xe, int p0,
                                             int lane) {
   const int R = p.R;
-  const int i0 = xs - 2 * R - 1;     // lead-in start (zero state, empty window)
+  const int lead = 2 * R + 1;        // lead-in: zero state, empty window, 2W+1 entering samples
   const int P0 = xs - R;             // first position of both streams
-  float2 S0[NPG], S[NPG][kO1K - 1], D[NPG][kO1K - 1], Ep[NPG], Lp[NPG];
+  RowO1State<NPG> st;
 #pragma unroll
   for (int q = 0; q < NPG; q++) {
-    S0[q] = Ep[q] = Lp[q] = make_float2(0.f, 0.f);
+    st.S0[q] = st.Ep[q] = st.Lp[q] = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int t = 0; t < kO1K - 1; t++) S[q][t] = D[q][t] = make_float2(0.f, 0.f);
+    for (int t = 0; t < kO1K - 1; t++) st.S[q][t] = st.D[q][t] = make_float2(0.f, 0.f);
   }
-  const long long pstride = (long long)p.in_rows * p.Wd;
-  float2* const dst0 = p.planes + b * p.planes_img_stride + (long long)p0 * pstride;
-  const int orow = lane >> 4, ocol = lane & 15;
+  const float* rowp = row_ptr(p, b, p.in_row0 + min(r0 + lane, p.in_rows - 1));
+  const bool vec = ((p.Wd & 3) == 0) && ((reinterpret_cast<uintptr_t>(rowp) & 15) == 0);
 
+  // ---- lead-in: windows xs-2W-1 .. xs-1 (leaving samples are still zero)
 #pragma unroll 1
-  for (int i = i0; i < xe; i++) {
-    const int s = i - i0, sl = i - xs;
-    if ((s & (kO1CH - 1)) == 0) o1_stage_f(p, sm.fin, b, r0, P0 + s, lane);
-    if (sl >= 0 && (sl & (kO1CH - 1)) == 0) o1_stage_f(p, sm.fout, b, r0, P0 + sl, lane);
-    float a2e, a2l;
-    float2 pe = o1_psi0(p, sm.fin[s & (kO1CH - 1)][lane], p0, a2e);
-    float2 pl = sl >= 0 ? o1_psi0(p, sm.fout[sl & (kO1CH - 1)][lane], p0, a2l) : make_float2(0.f, 0.f);
-    if (sl < 0) a2l = 0.f;
+  for (int s = 0; s < lead; s++) {
+    const int pos = P0 + s;
+    if (s == 0 || (pos & (kO1CH - 1)) == 0) o1_stage_row(p, sm.fin, rowp, pos & ~(kO1CH - 1), lane, vec, p0);
+    const float2 ve = sm.fin[lane * kO1TS + (pos & (kO1CH - 1))];
+    float2 pe = make_float2(ve.x, ve.x * ve.y);
+    const float a2e = ve.y * ve.y;
 #pragma unroll
     for (int q = 0; q < NPG; q++) {
-      if (sl >= 0) {
-        // output at x = i: y = sum_q alpha_q S_q  (state of window i, before the update)
-        float2 y = f2mul(f2s(p.o1_alpha[0]), S0[q]);
-#pragma unroll
-        for (int t = 0; t < kO1K - 1; t++) y = f2fma(f2s(p.o1_alpha[t + 1]), S[q][t], y);
-        sm.o[q][sl & (kO1OC - 1)][lane] = y;
-      }
-      // update to window i+1: A = x(i+W+1) + x(i-W-1), B = x(i+W) + x(i-W)
-      const float2 A = f2add(pe, Lp[q]);
-      const float2 B = f2add(Ep[q], pl);
-      S0[q] = f2add(S0[q], f2sub(pe, pl));
-#pragma unroll
-      for (int t = 0; t < kO1K - 1; t++) {
-        float2 d = f2fma(f2s(p.o1_nk[t + 1]), S[q][t], D[q][t]);
-        d = f2fma(f2s(p.o1_a[t + 1]), A, d);
-        d = f2fma(f2s(p.o1_nb[t + 1]), B, d);
-        D[q][t] = d;
-        S[q][t] = f2add(S[q][t], d);
-      }
-      Ep[q] = pe;
-      Lp[q] = pl;
+      o1_update(p, st.S0[q], st.S[q], st.D[q], pe, st.Ep[q], pe, make_float2(0.f, 0.f));
+      st.Ep[q] = pe;
       pe = f2mul(pe, f2s(a2e));
-      pl = f2mul(pl, f2s(a2l));
     }
-    // store a full chunk of 16 positions x 32 rows per pair (128-byte row segments)
-    if (sl >= 0 && ((sl & (kO1OC - 1)) == kO1OC - 1 || i == xe - 1)) {
-      __syncwarp();
-      const int xc = xs + (sl & ~(kO1OC - 1));
-      const int x = xc + ocol;
+  }
+  // ---- outputs x = xs .. xe-1, in chunks of 8 positions (xs is a multiple of 32)
+  o1_stage_row(p, sm.fout, rowp, (xs - R) & ~(kO1CH - 1), lane, vec, p0);
+  const long long pstride = (long long)p.in_rows * p.Wd;
+  const int orow = lane >> 3, ocol = lane & 7;
+  const int rows_left = p.in_rows - (r0 + orow);            // rows r0+orow+4j valid for 4j < rows_left
+  float2* const obase = p.planes + b * p.planes_img_stride + (long long)p0 * pstride +
+                        (long long)(r0 + orow) * p.Wd + ocol;
+#pragma unroll 1
+  for (int x = xs; x < xe; x += kO1OC) {
+    const int nb = min(kO1OC, xe - x);
+#pragma unroll 1
+    for (int j = 0; j < nb; j++) row_o1_step<NPG>(p, sm, st, x + j, j, rowp, vec, p0, lane);
+    // store the chunk: per pair, 8 positions x 32 rows (4 rows x 64 bytes per instruction)
+    __syncwarp();
+    if (ocol < nb) {
+      float2* o = obase + x;
 #pragma unroll
       for (int q = 0; q < NPG; q++) {
-#pragma unroll 4
-        for (int j = 0; j < 16; j++) {
-          const int rr = 2 * j + orow;
-          const int y = r0 + rr;
-          if (y < p.in_rows && x < xe) dst0[q * pstride + (long long)y * p.Wd + x] = sm.o[q][ocol][rr];
-        }
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+          if (4 * j < rows_left) o[(long long)(4 * j) * p.Wd] = sm.o[q][ocol][4 * j + orow];
+        o += pstride;
       }
-      __syncwarp();
     }
+    __syncwarp();
   }
 }
 
-__global__ void __launch_bounds__(32 * kO1Warps, 2) k_row_o1(const KParams p) {
+__global__ void __launch_bounds__(32 * kO1Warps, 3) k_row_o1(const KParams p) {
   extern __shared__ float4 smem_o1r[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   RowO1Smem& sm = reinterpret_cast<RowO1Smem*>(smem_o1r)[warp];
@@ -177,10 +236,32 @@ __global__ void __launch_bounds__(32 * kO1Warps, 2) k_row_o1(const KParams p) {
 
 // ------------------------------------------------------------------ column pass + eqs. (8)-(10)
 
+constexpr int kO1D = 4;          // column pass: cp.async pipeline depth (rows in flight)
+constexpr int kO1ColNPGMax = 5;
+
+struct ColO1Smem {
+  float2 ring[kO1D][2][kO1ColNPGMax][32];   // [stage][enter/leave][pair][lane]
+  float fring[kO1D][32];                    // f at the output row
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 template <int NPG, int G>
 __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const KParams p) {
   constexpr int CW = 32 / G;                       // columns per warp
+  extern __shared__ float4 smem_o1c[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  ColO1Smem& sm = reinterpret_cast<ColO1Smem*>(smem_o1c)[warp];
   const int ncb = (p.Wd + CW - 1) / CW;
   const int ntask = ncb * p.o1_nseg_y * p.B;
   const int task = blockIdx.x * kO1Warps + warp;
@@ -194,6 +275,7 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const KParams p) {
   const int xc = xok ? x : p.Wd - 1;
   const int ys = sy * p.o1_seg_y, ye = min(ys + p.o1_seg_y, p.out_rows);
   const int R = p.R;
+  const int lead = 2 * R + 1;
   const int p0 = g * NPG;
   const long long pstride = (long long)p.in_rows * p.Wd;
   const float2* const src = p.planes + b * p.planes_img_stride + (long long)p0 * pstride + xc;
@@ -212,58 +294,77 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const KParams p) {
 #pragma unroll
     for (int t = 0; t < kO1K - 1; t++) S[q][t] = D[q][t] = make_float2(0.f, 0.f);
   }
-  const int i0 = ys - 2 * R - 1;
-  auto prow = [&](int r) {                         // plane-buffer row of output-relative row r
-    return mirror(p.out_row0 + r, p.H) - p.in_row0;
-  };
-  // loads for step i: entering row i+R+1, leaving row i-R (zero during the lead-in), f(i)
-  float2 En[NPG], Ln[NPG];
-  float fn = 0.f;
-  auto load = [&](int i) {
-    const long long re = (long long)prow(i + R + 1) * p.Wd;
-    const bool lv = i >= ys;
-    const long long rl = lv ? (long long)prow(i - R) * p.Wd : 0;
+  // padding pairs (p0 + q >= NP) read zeros: their ring entries are never written
+#pragma unroll
+  for (int st = 0; st < kO1D; st++)
+#pragma unroll
+    for (int q = 0; q < NPG; q++)
+      if (q >= npl) sm.ring[st][0][q][lane] = sm.ring[st][1][q][lane] = make_float2(0.f, 0.f);
+
+  const bool fseg = p.seg[0].rows > 0 && p.out_row0 >= p.seg[0].row0 &&
+                    p.out_row0 + p.out_rows <= p.seg[0].row0 + p.seg[0].rows;
+  const float* const frow = p.seg[0].ptr + b * p.seg_img_stride +
+                            (long long)(p.out_row0 - p.seg[0].row0) * p.Wd + xc;
+  // step i (window centred on output-relative row i): entering row i+R+1, leaving row i-R
+  auto issue = [&](int i, int st) {
+    const long long re = (long long)(mirror(p.out_row0 + i + R + 1, p.H) - p.in_row0) * p.Wd;
+    // (during the lead-in the leaving sample is masked to zero; read a valid row instead)
+    const long long rl = i >= ys ? (long long)(mirror(p.out_row0 + i - R, p.H) - p.in_row0) * p.Wd : re;
 #pragma unroll
     for (int q = 0; q < NPG; q++) {
-      En[q] = q < npl ? __ldg(src + q * pstride + re) : make_float2(0.f, 0.f);
-      Ln[q] = (q < npl && lv) ? __ldg(src + q * pstride + rl) : make_float2(0.f, 0.f);
+      if (q < npl) {
+        cp_async8(&sm.ring[st][0][q][lane], src + q * pstride + re);
+        cp_async8(&sm.ring[st][1][q][lane], src + q * pstride + rl);
+      }
     }
-    fn = lv ? __ldg(row_ptr(p, b, p.out_row0 + i) + xc) : 0.f;
+    const int fi = max(i, 0);
+    cp_async4(&sm.fring[st][lane], fseg ? frow + (long long)fi * p.Wd : row_ptr(p, b, p.out_row0 + fi) + xc);
   };
-  load(i0);
+  const int i0 = ys - lead;
+#pragma unroll
+  for (int k = 0; k < kO1D - 1; k++) {
+    if (i0 + k < ye) issue(i0 + k, k);
+    cp_commit();
+  }
+  float* const outp = p.out + b * p.out_img_stride + x;
 #pragma unroll 1
   for (int i = i0; i < ye; i++) {
+    const int k = i - i0;
+    if (i + kO1D - 1 < ye) issue(i + kO1D - 1, (k + kO1D - 1) % kO1D);
+    cp_commit();
+    cp_wait<kO1D - 1>();                            // this lane's copies for step i landed
+    const int st = k % kO1D;
     float2 pe[NPG], pl[NPG];
+    const bool live = i >= ys;                      // lead-in: leaving samples are zero
 #pragma unroll
     for (int q = 0; q < NPG; q++) {
-      pe[q] = En[q];
-      pl[q] = Ln[q];
+      pe[q] = sm.ring[st][0][q][lane];
+      pl[q] = live ? sm.ring[st][1][q][lane] : make_float2(0.f, 0.f);
     }
-    const float fo = fn;
-    if (i + 1 < ye) load(i + 1);
-    if (i >= ys) {
-      // filtered pairs at row i, then partial P', Q' over this group's planes (eqs. 8-9)
-      float a = 0.f, e;
-      if (!p.raw) centre(p, fo, a, e);
+    if (live) {
+      const float fo = sm.fring[st][lane];
+      // filtered pairs at row i, partial P', Q' over this group's planes (eqs. 8-9)
+      const float a = p.raw ? 0.f : centre_a(p, fo);
       const float a2 = a * a;
-      float pw = 1.f, vprev = 0.f;                  // a'^{2 p0};  v_{2p0-1} = chat_{2p0-1} a'^{2p0-1}
-      if (p0 > 0) {
-        float po = 1.f, base = a;
-        for (int k = 2 * p0 - 1; k; k >>= 1) {      // binary powering (p0 is lane-group uniform)
-          if (k & 1) po *= base;
-          base *= base;
-        }
-        vprev = cprev * po;
-        pw = po * a;
+      float pwg = 1.f;                                // a'^{2 NPG}: one group's power step
+#pragma unroll
+      for (int kk = 0; kk < NPG; kk++) pwg *= a2;
+      float pw = 1.f, pwprev = 1.f;                   // a'^{2 p0} = pwg^g; a'^{2 (p0 - NPG)}
+#pragma unroll
+      for (int kk = 1; kk < G; kk++) {
+        pwprev = kk < g ? pwprev * pwg : pwprev;
+        pw = kk <= g ? pw * pwg : pw;
       }
+      float aodd = a;                                 // a'^{2 NPG - 1}
+#pragma unroll
+      for (int kk = 1; kk < NPG; kk++) aodd *= a2;
       float2 Q2 = make_float2(0.f, 0.f), P2 = make_float2(0.f, 0.f);
       float2 pw2 = make_float2(pw, pw * a);
+      float vprev = cprev * (pwprev * aodd);          // chat_{2p0-1} a'^{2p0-1} (0 for g = 0)
       float out_raw = 0.f;
 #pragma unroll
       for (int q = 0; q < NPG; q++) {
-        float2 y = f2mul(f2s(p.o1_alpha[0]), S0[q]);
-#pragma unroll
-        for (int t = 0; t < kO1K - 1; t++) y = f2fma(f2s(p.o1_alpha[t + 1]), S[q][t], y);
+        const float2 y = o1_output(p, S0[q], S[q]);
         if (q == 0) out_raw = y.x;
         const float2 v = f2mul(cq[q], pw2);
         Q2 = f2fma(v, y, Q2);
@@ -282,32 +383,23 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const KParams p) {
         if (p.raw) {
           o = out_raw;
         } else if (Q > 0.f && isfinite(Q) && isfinite(P)) {
-          o = p.t_c + p.t_h * (P / Q);                     // eq. (10) + uncentring
-        } else {                                           // guard (R8)
+          o = p.t_c + p.t_h * __fdividef(P, Q);          // eq. (10) + uncentring
+        } else {                                         // guard (R8)
           o = fminf(fmaxf(fo, p.L), p.U);
           if (p.fallback) atomicAdd(p.fallback, 1ull);
         }
-        p.out[b * p.out_img_stride + (long long)i * p.Wd + x] = o;
+        outp[(long long)i * p.Wd] = o;
       }
     }
     // update to window i+1
 #pragma unroll
     for (int q = 0; q < NPG; q++) {
-      const float2 A = f2add(pe[q], Lp[q]);
-      const float2 B = f2add(Ep[q], pl[q]);
-      S0[q] = f2add(S0[q], f2sub(pe[q], pl[q]));
-#pragma unroll
-      for (int t = 0; t < kO1K - 1; t++) {
-        float2 d = f2fma(f2s(p.o1_nk[t + 1]), S[q][t], D[q][t]);
-        d = f2fma(f2s(p.o1_a[t + 1]), A, d);
-        d = f2fma(f2s(p.o1_nb[t + 1]), B, d);
-        D[q][t] = d;
-        S[q][t] = f2add(S[q][t], d);
-      }
+      o1_update(p, S0[q], S[q], D[q], f2add(pe[q], Lp[q]), f2add(Ep[q], pl[q]), pe[q], pl[q]);
       Ep[q] = pe[q];
       Lp[q] = pl[q];
     }
   }
+  cp_wait<0>();
 }
 
 // ------------------------------------------------------------------ dispatch
@@ -319,7 +411,7 @@ cudaError_t launch_col(const KParams& p, cudaStream_t s) {
   constexpr int CW = 32 / G;
   const long long nt = (long long)((p.Wd + CW - 1) / CW) * p.o1_nseg_y * p.B;
   const unsigned grid = (unsigned)((nt + kO1Warps - 1) / kO1Warps);
-  k_col_o1<NPG, G><<<grid, 32 * kO1Warps, 0, s>>>(p);
+  k_col_o1<NPG, G><<<grid, 32 * kO1Warps, kO1Warps * sizeof(ColO1Smem), s>>>(p);
   return cudaGetLastError();
 }
 

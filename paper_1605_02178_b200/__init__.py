@@ -212,14 +212,14 @@ def bilateral_c(img, sigma_s, sigma_r, N, c, out=None, stream=None):
 
 
 def filter_host(img: np.ndarray, sigma_s, sigma_r, N, c=None, L=0.0, U=255.0, out: np.ndarray | None = None,
-                stream=None):
+                stream=None, op=OP_AUTO):
     """gc_filter_host: host float32 arrays in and out (pinned recommended); synchronous."""
     if img.dtype != np.float32 or not img.flags.c_contiguous:
         raise TypeError("img must be a C-contiguous float32 array")
     shape = img.shape
     B, H, W = (1, *shape) if img.ndim == 2 else shape
     out = np.empty_like(img) if out is None else out
-    p, keep = _params(N, sigma_s, sigma_r, L, U, c)
+    p, keep = _params(N, sigma_s, sigma_r, L, U, c, op)
     _check(_lib().gc_filter_host(ctypes.c_void_p(img.ctypes.data), B, H, W, ctypes.byref(p),
                                  ctypes.c_void_p(out.ctypes.data), _stream(stream)), "gc_filter_host")
     del keep

@@ -49,6 +49,12 @@ __device__ __forceinline__ float2 f2sub(float2 a, float2 b) {
 
 __device__ __forceinline__ float2 f2s(float s) { return make_float2(s, s); }
 
+// Programmatic dependent launch (PDL): the column pass is launched while the row pass
+// drains; it waits here (all of the row pass complete and visible) before reading planes.
+// Both are no-ops when the launch did not use the PDL attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Whole-sample symmetric extension (R5): period 2n-2, n = 1 -> 0.
 static __device__ __noinline__ int mirror_slow(int p, int n) {
   if (n <= 1) return 0;

@@ -60,6 +60,7 @@ struct RowCfg {
 template <int W>
 __global__ void __launch_bounds__(32 * kRowWarpsPerCta, 16) k_row_t(const KParams p, unsigned* col_task_ctr) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *col_task_ctr = 0u;   // consumed by k_col_t (stream-ordered)
+  pdl_trigger();
   using C = RowCfg<W>;
   constexpr int RX = C::RX;
   extern __shared__ float4 smem_row[];
@@ -242,8 +243,10 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 3)
     k_col_t(const __grid_constant__ CUtensorMap tmap, const KParams p, unsigned* task_ctr) {
   using C = ColCfg<W>;
   constexpr int RY = C::RY;
-  extern __shared__ float4 smem_col[];
-  char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_col) + 127) & ~uintptr_t(127));
+  // dynamic shared memory starts at offset 0 of the CTA's window (no static smem here), so it
+  // is 1024-byte aligned; no integer arithmetic on the pointer, so every access stays LDS/STS
+  extern __shared__ __align__(1024) float4 smem_col[];
+  char* base = reinterpret_cast<char*>(smem_col);
   float2* sB = reinterpret_cast<float2*>(base);                                         // [S][NJ][32]
   unsigned long long* full = reinterpret_cast<unsigned long long*>(base + kColStages * C::BUFB);
   unsigned long long* empty = full + kColStages;
@@ -264,6 +267,7 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 3)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();                                     // planes and task counter from k_row_t
 
   if (warp == kColConsumers) {
     // ------------------------------------------------ producer warp: fetch tasks dynamically,
@@ -414,6 +418,7 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 3)
 
 // Row pass for any radius: plane pairs staged in shared memory one pair at a time.
 __global__ void __launch_bounds__(256) k_row_rt(const KParams p) {
+  pdl_trigger();
   constexpr int TX = 64, TY = 4;
   extern __shared__ float4 smem_rt[];
   const int R = p.R;
@@ -454,6 +459,7 @@ __global__ void __launch_bounds__(256) k_row_rt(const KParams p) {
 
 // Column pass + recombination for any radius: one output pixel per thread.
 __global__ void __launch_bounds__(256) k_col_rt(const KParams p) {
+  pdl_wait();
   const int b = blockIdx.z;
   const int x = blockIdx.x * 32 + threadIdx.x % 32;
   const int y = blockIdx.y * 8 + threadIdx.x / 32;
@@ -549,8 +555,8 @@ cudaError_t launch_t(const KParams& p, cudaStream_t s) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (p.ev[1]) cudaEventRecord(p.ev[1], s);
-  kc<<<(unsigned)gc, 32 * (kColConsumers + 1), smem_c, s>>>(map, p, p.counters);
-  e = cudaGetLastError();
+  e = launch_k(kc, dim3((unsigned)gc), dim3(32 * (kColConsumers + 1)), smem_c, s, p.ev[1] == nullptr, map, p,
+               p.counters);
   if (p.ev[2]) cudaEventRecord(p.ev[2], s);
   return e;
 }
@@ -578,8 +584,7 @@ cudaError_t launch_rt(const KParams& p, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   if (p.ev[1]) cudaEventRecord(p.ev[1], s);
   dim3 gc((p.Wd + 31) / 32, (p.out_rows + 7) / 8, p.B);
-  k_col_rt<<<gc, 256, 0, s>>>(p);
-  e = cudaGetLastError();
+  e = launch_k(k_col_rt, gc, dim3(256), 0, s, p.ev[1] == nullptr, p);
   if (p.ev[2]) cudaEventRecord(p.ev[2], s);
   return e;
 }

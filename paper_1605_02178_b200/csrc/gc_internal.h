@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 
 #include "../../include/gc.h"
 
@@ -80,6 +81,25 @@ struct O1Fit {
   double fit_err;
 };
 const O1Fit& o1_fit_cached(float sigma_s);
+
+// Launch `kernel` on `s`; with pdl = true the launch carries the programmatic-stream-
+// serialization attribute (its prologue overlaps the previous kernel's tail; the kernel
+// calls pdl_wait() before consuming that kernel's output).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Launch the two-pass FIR pipeline (row pass + column pass with recombination) on
 // `stream`.  Scratch (the plane buffer) must already be in p.planes.

@@ -213,6 +213,7 @@ __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int
 
 __global__ void __launch_bounds__(32 * kO1Warps, 3) k_row_o1(const KParams p) {
   extern __shared__ float4 smem_o1r[];
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   RowO1Smem& sm = reinterpret_cast<RowO1Smem*>(smem_o1r)[warp];
   const int nrb = (p.in_rows + 31) / 32;
@@ -301,6 +302,7 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const KParams p) {
     for (int q = 0; q < NPG; q++)
       if (q >= npl) sm.ring[st][0][q][lane] = sm.ring[st][1][q][lane] = make_float2(0.f, 0.f);
 
+  pdl_wait();                                       // planes from k_row_o1
   const bool fseg = p.seg[0].rows > 0 && p.out_row0 >= p.seg[0].row0 &&
                     p.out_row0 + p.out_rows <= p.seg[0].row0 + p.seg[0].rows;
   const float* const frow = p.seg[0].ptr + b * p.seg_img_stride +
@@ -411,8 +413,8 @@ cudaError_t launch_col(const KParams& p, cudaStream_t s) {
   constexpr int CW = 32 / G;
   const long long nt = (long long)((p.Wd + CW - 1) / CW) * p.o1_nseg_y * p.B;
   const unsigned grid = (unsigned)((nt + kO1Warps - 1) / kO1Warps);
-  k_col_o1<NPG, G><<<grid, 32 * kO1Warps, kO1Warps * sizeof(ColO1Smem), s>>>(p);
-  return cudaGetLastError();
+  return launch_k(k_col_o1<NPG, G>, dim3(grid), dim3(32 * kO1Warps), kO1Warps * sizeof(ColO1Smem), s,
+                  p.ev[1] == nullptr, p);
 }
 
 template <int G>

@@ -339,7 +339,8 @@ def main():
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             try:
-                traffic = json.load(open(tp)).get(f"{cfg.name}:{dom}")
+                key = f"{cfg.name}_s{sigma_s:g}_{'o1' if op == 2 else 'fir'}:{dom}"
+                traffic = json.load(open(tp)).get(key)
             except Exception:
                 traffic = None
         roof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",

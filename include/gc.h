@@ -153,6 +153,18 @@ gc_status gc_gaussian(const float* imgs, int B, int H, int W, float sigma_s, int
                       void* stream);
 
 /*
+ * gc_bilateral_direct — the direct bilateral filter of eq. (1), the O(sigma_s^2)
+ * filter the GCF approximates: B images [B][H][W] fp32 on the device, Omega = [-W_s, W_s]^2,
+ * W_s = ceil(3 sigma_s), whole-sample symmetric extension, Gaussian spatial and
+ * range kernels, fp32 arithmetic (one exp per tap; cost (2 W_s + 1)^2 per pixel).  A reference
+ * for full-image MSE / PSNR of the fast filter; not on the GCF hot path.
+ * Errors: GC_EINVAL (sizes, sigmas, null or overlapping pointers), GC_ERANGE (W_s > 1024),
+ * GC_ECUDA.
+ */
+gc_status gc_bilateral_direct(const float* imgs, int B, int H, int W, float sigma_s, float sigma_r,
+                              float* outs, void* stream);
+
+/*
  * gc_operator_taps — host only, pure: the 1-D impulse response k[m], m = -W_s..W_s, that
  * operator `op` applies along each axis at sigma_s (GC_OP_FIR: the normalised sampled taps of
  * eq. 7; GC_OP_O1: the cosine expansion the O(1) kernels evaluate; GC_OP_AUTO: whichever

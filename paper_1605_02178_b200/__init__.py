@@ -17,7 +17,7 @@ import numpy as np
 __all__ = [
     "GCError", "lib", "coeffs", "bilateral", "bilateral_batch", "bilateral_c", "filter",
     "filter_host", "filter_window", "band_plan", "Comm", "bilateral_band", "version",
-    "OP_AUTO", "OP_FIR", "OP_O1", "gaussian", "operator_taps",
+    "OP_AUTO", "OP_FIR", "OP_O1", "gaussian", "operator_taps", "bilateral_direct",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -71,6 +71,7 @@ def _lib():
         L.gc_filter_host.argtypes = [vp, i, i, i, ctypes.POINTER(_Params), vp, vp]
         L.gc_filter_window.argtypes = [ctypes.POINTER(vp), ip, ip, i, i, i, i, ctypes.POINTER(_Params), vp, vp]
         L.gc_gaussian.argtypes = [vp, i, i, i, f, i, vp, vp]
+        L.gc_bilateral_direct.argtypes = [vp, i, i, i, f, f, vp, vp]
         L.gc_operator_taps.argtypes = [f, i, ctypes.POINTER(d), ip]
         L.gc_band_plan.argtypes = [i, i, i, ip, f, ip, ip, ip, ip, ip]
         L.gc_comm_unique_id.argtypes = [ctypes.c_char_p]
@@ -79,7 +80,8 @@ def _lib():
         L.gc_bilateral_band.argtypes = [vp, i, i, i, i, ctypes.POINTER(_Params), vp, vp, vp]
         for name in ["gc_coeffs", "gc_bilateral", "gc_bilateral_batch", "gc_bilateral_c", "gc_filter",
                      "gc_filter_host", "gc_filter_window", "gc_band_plan", "gc_comm_unique_id",
-                     "gc_comm_init", "gc_comm_destroy", "gc_bilateral_band", "gc_gaussian", "gc_operator_taps"]:
+                     "gc_comm_init", "gc_comm_destroy", "gc_bilateral_band", "gc_gaussian", "gc_operator_taps",
+                     "gc_bilateral_direct"]:
             getattr(L, name).restype = ctypes.c_int
         _LIB = L
     return _LIB
@@ -168,6 +170,21 @@ def gaussian(img, sigma_s, op=OP_AUTO, out=None, stream=None):
     out = torch.empty_like(img) if out is None else out
     _check(_lib().gc_gaussian(_dev_f32(img, "img"), B, H, W, float(sigma_s), int(op), _dev_f32(out, "out"),
                               _stream(stream)), "gc_gaussian")
+    return out
+
+
+def bilateral_direct(img, sigma_s, sigma_r, out=None, stream=None):
+    """gc_bilateral_direct: eq. (1) itself on a [H, W] or [B, H, W] float32 CUDA tensor (reference)."""
+    import torch
+    if img.dim() == 2:
+        B, (H, W) = 1, img.shape
+    elif img.dim() == 3:
+        B, H, W = img.shape
+    else:
+        raise ValueError("img must be [H, W] or [B, H, W]")
+    out = torch.empty_like(img) if out is None else out
+    _check(_lib().gc_bilateral_direct(_dev_f32(img, "img"), B, H, W, float(sigma_s), float(sigma_r),
+                                      _dev_f32(out, "out"), _stream(stream)), "gc_bilateral_direct")
     return out
 
 

@@ -335,6 +335,17 @@ gc_status gc_gaussian(const float* imgs, int B, int H, int W, float sigma_s, int
   return run(k, taps_host, reinterpret_cast<cudaStream_t>(stream));
 }
 
+gc_status gc_bilateral_direct(const float* imgs, int B, int H, int W, float sigma_s, float sigma_r, float* outs,
+                              void* stream) {
+  if (!imgs || !outs || B < 1 || H < 1 || W < 1) return GC_EINVAL;
+  if (!finite_pos(sigma_s) || !finite_pos(sigma_r)) return GC_EINVAL;
+  const size_t bytes = (size_t)B * H * W * sizeof(float);
+  if (overlap(imgs, bytes, outs, bytes)) return GC_EINVAL;
+  const int R = radius_of(sigma_s);
+  if (R > kMaxFirW) return GC_ERANGE;
+  return cuda_status(launch_direct(imgs, B, H, W, R, sigma_s, sigma_r, outs, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 gc_status gc_operator_taps(float sigma_s, int op, double* taps_out, int* W_out) {
   if (!std::isfinite(sigma_s) || !(sigma_s > 0)) return GC_EINVAL;
   if (op != GC_OP_AUTO && op != GC_OP_FIR && op != GC_OP_O1) return GC_EINVAL;

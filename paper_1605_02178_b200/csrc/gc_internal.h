@@ -108,4 +108,8 @@ cudaError_t launch_fir_two_pass(const KParams& p, cudaStream_t stream);
 // Launch the two-pass O(1) exact-window pipeline (gc_o1.cu).  Same buffers and semantics.
 cudaError_t launch_o1_two_pass(const KParams& p, cudaStream_t stream);
 
+// Direct bilateral filter of eq. (1) (gc_direct.cu).
+cudaError_t launch_direct(const float* img, int B, int H, int W, int R, float sigma_s, float sigma_r, float* out,
+                          cudaStream_t s);
+
 }  // namespace gc

@@ -96,6 +96,9 @@ def test_device_entry_points_validate_before_cuda(gc):
     assert lib.gc_gaussian(fake, 1, 8, 8, 2.0, 7, fake2, None) == 1               # unknown operator
     assert lib.gc_gaussian(fake, 1, 8, 8, 500.0, 1, fake2, None) == 2             # W_s > FIR limit
     assert lib.gc_gaussian(fake, 1, 8, 8, 2.0, 1, fake, None) == 1                # aliased
+    assert lib.gc_bilateral_direct(None, 1, 8, 8, 2.0, 30.0, fake2, None) == 1
+    assert lib.gc_bilateral_direct(fake, 1, 8, 8, 2.0, 0.0, fake2, None) == 1
+    assert lib.gc_bilateral_direct(fake, 1, 8, 8, 500.0, 30.0, fake2, None) == 2  # W_s > 1024
 
 
 def test_status_strings(gc):

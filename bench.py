@@ -48,6 +48,7 @@ def _args():
     a.add_argument("--batch", type=int, default=None, help="override the batch size (profiling only)")
     a.add_argument("--no-cpu-baseline", action="store_true")
     a.add_argument("--op", type=int, default=0, choices=[0, 1, 2], help="0 auto, 1 FIR, 2 O(1)")
+    a.add_argument("--fp64", action="store_true", help="binary64 internal arithmetic (GC_PREC_FP64)")
     return a.parse_args()
 
 
@@ -240,7 +241,7 @@ def main():
         if comm is not None:
             gc.bilateral_band(x, cfg.H, row0, sigma_s, sigma_r, cfg.N, comm, out=out, op=args.op)
         else:
-            gc.filter(x, sigma_s, sigma_r, cfg.N, out=out, events=events, op=args.op)
+            gc.filter(x, sigma_s, sigma_r, cfg.N, out=out, events=events, op=args.op, fp64=args.fp64)
 
     for _ in range(args.warmup):
         if flush is not None:
@@ -294,7 +295,7 @@ def main():
 
     # ---- e2e: same metric through gc_filter_host with pinned host buffers
     e2e = None
-    if not args.no_e2e and comm is None:
+    if not args.no_e2e and comm is None and not args.fp64:
         hin = torch.from_numpy(x.cpu().numpy()).pin_memory()
         hout = torch.empty_like(hin).pin_memory()
         hin_np, hout_np = hin.numpy(), hout.numpy()
@@ -327,7 +328,7 @@ def main():
     # ---- roofline of the dominant kernel (FP32 ALU bound)
     roof = None
     kernels = None
-    if row_ms is not None:
+    if row_ms is not None and not args.fp64:      # (fp64 mode: a correctness instrument, no roofline)
         op = resolve_op(args.op, R)
         fr = flops_row(cfg.N, R, B * H * W, op)   # whole-image row pass (in_rows = H)
         fc = flops_col(cfg.N, R, B * H * W, op)
@@ -352,7 +353,7 @@ def main():
     hbm["frac_of_measured"] = hbm["achieved_GBps"] / 6550.7
     line = {"metric": METRIC, "value": value, "unit": "MP/s", "n_gpus": ws, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if cfg.name in ("c4", "c5") else "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong" if cfg.name in ("c4", "c5") else "weak", "vs_baseline": None, "dtype": "f64" if args.fp64 else "f32",
             "data": "synthetic (seeded, synth/images.py)", "config": _config(cfg, sigma_s, sigma_r, ws),
             "roofline": roof, "kernels": kernels, "hbm": hbm, "e2e": e2e,
             "gpu_launches": 2 * K, "clocks": clk.summary(), "impl": "ours", "lib": gc.version()}

@@ -121,10 +121,16 @@ typedef struct gc_params {
   void* events[3];                    /* NULL or cudaEvent_t recorded on `stream` before
                                          the row pass, between the passes and after the
                                          column pass (per-kernel timing for bench.py)      */
+  int precision;                      /* GC_PREC_FP32 (default) or GC_PREC_FP64: planes,
+                                         eq. (7) and eqs. (8)-(10) in binary64 (FIR
+                                         operator, W_s <= 1024; input/output stay fp32)    */
 } gc_params;
 
+#define GC_PREC_FP32 0
+#define GC_PREC_FP64 1
+
 /* Fill p with the defaults: L=0, U=255, c=NULL, op=GC_OP_AUTO, fallback_count=NULL,
-   events={NULL}. */
+   events={NULL}, precision=GC_PREC_FP32. */
 void gc_params_init(gc_params* p, int N, float sigma_s, float sigma_r);
 
 /* B images [B][H][W] on the device (B >= 1). Errors as gc_bilateral. */

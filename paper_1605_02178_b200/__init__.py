@@ -24,6 +24,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgc.so")
 
 OP_AUTO, OP_FIR, OP_O1 = 0, 1, 2
+PREC_FP32, PREC_FP64 = 0, 1
 _STATUS = {0: "GC_OK", 1: "GC_EINVAL", 2: "GC_ERANGE", 3: "GC_ECUDA", 4: "GC_ENOMEM", 5: "GC_ENCCL"}
 
 
@@ -44,6 +45,7 @@ class _Params(ctypes.Structure):
         ("op", ctypes.c_int),
         ("fallback_count", ctypes.c_void_p),
         ("events", ctypes.c_void_p * 3),
+        ("precision", ctypes.c_int),
     ]
 
 
@@ -107,10 +109,11 @@ def coeffs(N: int, sigma_r: float, L: float = 0.0, U: float = 255.0):
     return np.array(c[:], dtype=np.float64), mu.value
 
 
-def _params(N, sigma_s, sigma_r, L=0.0, U=255.0, c=None, op=OP_AUTO, fallback=None, events=None):
+def _params(N, sigma_s, sigma_r, L=0.0, U=255.0, c=None, op=OP_AUTO, fallback=None, events=None, fp64=False):
     p = _Params()
     _lib().gc_params_init(ctypes.byref(p), int(N), float(sigma_s), float(sigma_r))
     p.L, p.U, p.op = float(L), float(U), int(op)
+    p.precision = PREC_FP64 if fp64 else PREC_FP32
     keep = None
     if c is not None:
         keep = (ctypes.c_double * (N + 1))(*[float(v) for v in c])
@@ -137,11 +140,12 @@ def _dev_f32(t, name):
 
 
 def filter(img, sigma_s, sigma_r, N, c=None, L=0.0, U=255.0, out=None, op=OP_AUTO, fallback=None, stream=None,
-           events=None):
+           events=None, fp64=False):
     """GCF of a [H, W] or [B, H, W] float32 CUDA tensor (gc_filter).  Asynchronous on `stream`.
 
     c: optional caller coefficients c_0..c_N (e.g. 1/n! = GPF); fallback: optional int64
-    CUDA tensor of one element that receives the number of guarded pixels (R8)."""
+    CUDA tensor of one element that receives the number of guarded pixels (R8); fp64: binary64
+    internal arithmetic (GC_PREC_FP64)."""
     import torch
     if img.dim() == 2:
         B, (H, W) = 1, img.shape
@@ -151,7 +155,7 @@ def filter(img, sigma_s, sigma_r, N, c=None, L=0.0, U=255.0, out=None, op=OP_AUT
         raise ValueError("img must be [H, W] or [B, H, W]")
     if out is None:
         out = torch.empty_like(img)
-    p, keep = _params(N, sigma_s, sigma_r, L, U, c, op, fallback, events)
+    p, keep = _params(N, sigma_s, sigma_r, L, U, c, op, fallback, events, fp64)
     _check(_lib().gc_filter(_dev_f32(img, "img"), B, H, W, ctypes.byref(p), _dev_f32(out, "out"), _stream(stream)),
            "gc_filter")
     del keep

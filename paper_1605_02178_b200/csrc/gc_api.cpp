@@ -74,7 +74,9 @@ gc_status validate_params(const gc_params* p) {
   if (!finite_pos(p->sigma_s) || !finite_pos(p->sigma_r)) return GC_EINVAL;
   if (!std::isfinite(p->L) || !std::isfinite(p->U) || !(p->U > p->L)) return GC_EINVAL;
   if (p->op != GC_OP_AUTO && p->op != GC_OP_FIR && p->op != GC_OP_O1) return GC_EINVAL;
-  if (radius_of(p->sigma_s) > (p->op == GC_OP_FIR ? kMaxFirW : kO1MaxW)) return GC_ERANGE;
+  if (p->precision != GC_PREC_FP32 && p->precision != GC_PREC_FP64) return GC_EINVAL;
+  if (radius_of(p->sigma_s) > (p->op == GC_OP_FIR || p->precision == GC_PREC_FP64 ? kMaxFirW : kO1MaxW))
+    return GC_ERANGE;
   if (p->c) {
     for (int n = 0; n <= p->N; n++)
       if (!std::isfinite(p->c[n])) return GC_EINVAL;
@@ -105,11 +107,20 @@ gc_status fill_constants(const gc_params* p, KParams& k, std::vector<float2>& ta
   }
   const int planes = ((p->N + 2) + 1) / 2 * 2;
   k.NP = planes / 2;
+  for (int n = 0; n < kMaxPlanes; n++) k.chat_d[n] = n <= p->N ? cm[n] : 0.0;
+  k.fp64 = p->precision == GC_PREC_FP64;
+  k.d_L = L;
+  k.d_U = U;
+  k.d_tc = 0.5 * (L + U);
+  k.d_th = th;
+  k.d_inv_th = 1.0 / th;
+  k.d_exk = -0.5 * mu;
   for (int q = 0; q < kMaxPairs; q++) {
     const int n0 = 2 * q, n1 = 2 * q + 1;
     k.chat2[q] = make_float2(n0 <= p->N ? (float)cm[n0] : 0.f, n1 <= p->N ? (float)cm[n1] : 0.f);
   }
   k.R = radius_of(p->sigma_s);
+  k.sigma_s_host = p->sigma_s;
   std::vector<double> t = taps_of(p->sigma_s, k.R);
   taps_host.resize(t.size());
   for (size_t m = 0; m < t.size(); m++) taps_host[m] = make_float2((float)t[m], (float)t[m]);
@@ -123,7 +134,8 @@ gc_status fill_constants(const gc_params* p, KParams& k, std::vector<float2>& ta
   k.fallback = p->fallback_count;
   for (int i = 0; i < 3; i++) k.ev[i] = reinterpret_cast<cudaEvent_t>(p->events[i]);
   // operator: GC_OP_AUTO = FIR for small radii (fewer instructions), O(1) above
-  const int op = p->op == GC_OP_AUTO ? (k.R >= kO1AutoMinW ? GC_OP_O1 : GC_OP_FIR) : p->op;
+  int op = p->op == GC_OP_AUTO ? (k.R >= kO1AutoMinW ? GC_OP_O1 : GC_OP_FIR) : p->op;
+  if (k.fp64) op = GC_OP_FIR;                     // binary64 mode: the exact FIR of eq. (7)
   k.op = op;
   if (op == GC_OP_O1) o1_constants(p->sigma_s, k);
   return GC_OK;
@@ -165,14 +177,23 @@ gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) 
   float2* planes = nullptr;
   float2* taps_dev = nullptr;
   // plane buffer + 256 bytes of task counters at its end
-  cudaError_t e = cudaMallocAsync((void**)&planes, plane_elems * k.B * sizeof(float2) + 256, s);
+  const size_t elem = k.fp64 ? sizeof(double2) : sizeof(float2);
+  cudaError_t e = cudaMallocAsync((void**)&planes, plane_elems * k.B * elem + 256, s);
   if (e != cudaSuccess) return cuda_status(e);
-  k.counters = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(planes) + plane_elems * k.B * sizeof(float2));
-  if (op == GC_OP_FIR && k.R > kMaxTemplW) {
-    e = cudaMallocAsync((void**)&taps_dev, taps_host.size() * sizeof(float2), s);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(taps_dev, taps_host.data(), taps_host.size() * sizeof(float2),
-                          cudaMemcpyHostToDevice, s);
+  k.counters = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(planes) + plane_elems * k.B * elem);
+  if (k.fp64 || (op == GC_OP_FIR && k.R > kMaxTemplW)) {
+    // taps for the runtime-radius kernels: (k_m, k_m) fp32 pairs, or k_m in binary64
+    std::vector<double> td;
+    const void* src = taps_host.data();
+    size_t bytes = taps_host.size() * sizeof(float2);
+    if (k.fp64) {
+      td = taps_of(k.sigma_s_host, k.R);
+      src = td.data();
+      bytes = td.size() * sizeof(double);
+    }
+    e = cudaMallocAsync((void**)&taps_dev, bytes, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(taps_dev, src, bytes, cudaMemcpyHostToDevice, s);
+    // (pageable source: cudaMemcpyAsync returns once the bytes are staged, td may then go)
     if (e != cudaSuccess) {
       cudaFreeAsync(planes, s);
       if (taps_dev) cudaFreeAsync(taps_dev, s);
@@ -182,7 +203,8 @@ gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) 
   k.planes = planes;
   k.planes_img_stride = (long long)plane_elems;
   k.taps_g = taps_dev;
-  e = op == GC_OP_O1 ? launch_o1_two_pass(k, s) : launch_fir_two_pass(k, s);
+  k.taps_d = reinterpret_cast<const double*>(taps_dev);
+  e = k.fp64 ? launch_fp64_two_pass(k, s) : op == GC_OP_O1 ? launch_o1_two_pass(k, s) : launch_fir_two_pass(k, s);
   cudaError_t e2 = cudaFreeAsync(planes, s);
   if (taps_dev) cudaFreeAsync(taps_dev, s);
   if (e != cudaSuccess) return cuda_status(e);

@@ -55,6 +55,14 @@ __device__ __forceinline__ float2 f2s(float s) { return make_float2(s, s); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Guard counter (R8): one atomic per warp instead of one per guarded pixel.
+// Every lane of `mask` must call it (lanes outside it are not counted).
+__device__ __forceinline__ void count_guarded(unsigned long long* ctr, unsigned mask, unsigned n) {
+  if (!ctr) return;
+  const unsigned tot = __reduce_add_sync(mask, n);
+  if (tot && (threadIdx.x & 31) == (unsigned)(__ffs(mask) - 1)) atomicAdd(ctr, (unsigned long long)tot);
+}
+
 // Whole-sample symmetric extension (R5): period 2n-2, n = 1 -> 0.
 static __device__ __noinline__ int mirror_slow(int p, int n) {
   if (n <= 1) return 0;

@@ -330,6 +330,7 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 3)
 
   // ------------------------------------------------ consumer warps
   const int seg = warp;
+  unsigned nguard = 0;                             // guarded outputs of this lane (R8)
   float fo[RY], av[RY], P[RY], Q[RY], vpy[RY], pwx[RY], raw0[RY];
   int b = 0, x = 0, y0 = 0;
   for (int k = 0;; k++) {
@@ -406,12 +407,13 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 3)
           o = p.t_c + p.t_h * (Pi / Qi);                 // eq. (10) + uncentring
         } else {                                          // guard (R8)
           o = fminf(fmaxf(fo[i], p.L), p.U);
-          if (p.fallback) atomicAdd(p.fallback, 1ull);
+          nguard++;
         }
         out[(long long)yy * p.Wd] = o;
       }
     }
   }
+  count_guarded(p.fallback, 0xffffffffu, nguard);
 }
 
 // ------------------------------------------------------------------ runtime-W kernels
@@ -489,14 +491,16 @@ __global__ void __launch_bounds__(256) k_col_rt(const KParams p) {
   }
   const float Q = Q2.x + Q2.y, P = P2.x + P2.y;
   float o;
+  unsigned guarded = 0;
   if (p.raw) {
     o = raw0;
   } else if (Q > 0.f && isfinite(Q) && isfinite(P)) {
     o = p.t_c + p.t_h * (P / Q);
   } else {
     o = fminf(fmaxf(f, p.L), p.U);
-    if (p.fallback) atomicAdd(p.fallback, 1ull);
+    guarded = 1;
   }
+  count_guarded(p.fallback, __activemask(), guarded);
   p.out[b * p.out_img_stride + (long long)y * p.Wd + x] = o;
 }
 

@@ -68,6 +68,12 @@ struct KParams {
   int o1_seg_y, o1_nseg_y;         // column pass: y-segment length and count
   int o1_groups;                   // row pass: plane-pair groups (<= 4 pairs each)
   int raw;                         // 1: eq. (7) of f itself (gc_gaussian): pair 0 = (f, 0), out = Fbar_0
+  // binary64 internal arithmetic (gc_fp64.cu; gc_params.precision = GC_PREC_FP64)
+  int fp64;
+  float sigma_s_host;                             // sigma_s (host side: taps)
+  double d_tc, d_th, d_inv_th, d_exk, d_L, d_U;   // d_exk = -mu/2 (natural exp)
+  const double* taps_d;                           // k_m, m = 0..2R (device)
+  double chat_d[kMaxPlanes];                      // chat_n, zero beyond N
 };
 
 // O(1) operator constants for radius R = ceil(3 sigma_s) (gc_api.cpp): least-squares K-term
@@ -107,6 +113,9 @@ cudaError_t launch_fir_two_pass(const KParams& p, cudaStream_t stream);
 
 // Launch the two-pass O(1) exact-window pipeline (gc_o1.cu).  Same buffers and semantics.
 cudaError_t launch_o1_two_pass(const KParams& p, cudaStream_t stream);
+
+// Two-pass FIR pipeline in binary64 (gc_fp64.cu): planes are double2 pairs (twice the bytes).
+cudaError_t launch_fp64_two_pass(const KParams& p, cudaStream_t stream);
 
 // Direct bilateral filter of eq. (1) (gc_direct.cu).
 cudaError_t launch_direct(const float* img, int B, int H, int W, int R, float sigma_s, float sigma_r, float* out,

@@ -329,6 +329,7 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const KParams p) {
     cp_commit();
   }
   float* const outp = p.out + b * p.out_img_stride + x;
+  unsigned nguard = 0;                              // guarded outputs of this lane (R8)
 #pragma unroll 1
   for (int i = i0; i < ye; i++) {
     const int k = i - i0;
@@ -388,7 +389,7 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const KParams p) {
           o = p.t_c + p.t_h * __fdividef(P, Q);          // eq. (10) + uncentring
         } else {                                         // guard (R8)
           o = fminf(fmaxf(fo, p.L), p.U);
-          if (p.fallback) atomicAdd(p.fallback, 1ull);
+          nguard++;
         }
         outp[(long long)i * p.Wd] = o;
       }
@@ -402,6 +403,7 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const KParams p) {
     }
   }
   cp_wait<0>();
+  count_guarded(p.fallback, 0xffffffffu, nguard);
 }
 
 // ------------------------------------------------------------------ dispatch

@@ -116,3 +116,42 @@ def test_o1_large_degree(gc):
     ref, _ = oracle.gc_filter(img, 6.0, 30.0, 40)
     out = gc.filter(t, 6.0, 30.0, 40, op=OP_O1).cpu().numpy().astype(np.float64)
     assert np.max(np.abs(out - ref)) <= MAX_ABS
+
+
+@pytest.mark.parametrize("op", [OP_FIR, OP_O1])
+def test_guard_counts_every_pixel(gc, op):
+    """Coefficients with c_0 < 0 and c_n = 0 otherwise give Q = c_0 Fbar_0 < 0 at every pixel:
+    the guard of DESIGN.md R8 must pass f through everywhere and count H*W exactly (the
+    counter is warp-aggregated in the kernels)."""
+    import torch
+    img = config_image("c2", H=133, W=257)
+    t = torch.from_numpy(img).cuda()
+    fb = torch.zeros(1, dtype=torch.int64, device="cuda")
+    c = np.zeros(7)
+    c[0] = -1.0
+    out = gc.filter(t, 5.0, 70.0, 6, c=c, op=op, fallback=fb)
+    torch.cuda.synchronize()
+    assert int(fb.item()) == img.size
+    assert np.array_equal(out.cpu().numpy(), img)
+
+
+def test_band_path_single_rank_nccl(gc):
+    """gc_bilateral_band through a real (one-rank) NCCL communicator: no neighbours, so the
+    band is the whole image and must equal gc_filter bit for bit."""
+    import os
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    comm = gc.Comm(0, 1)
+    img = config_image("c5", H=300, W=260)
+    t = torch.from_numpy(img).cuda()
+    for s in [3.0, 16.0]:
+        band = gc.bilateral_band(t, 300, 0, s, 55.0, 12, comm)
+        whole = gc.filter(t, s, 55.0, 12)
+        torch.cuda.synchronize()
+        assert torch.equal(band, whole)
+    comm.close()
+    dist.destroy_process_group()

@@ -62,8 +62,8 @@ void o1_segments(KParams& k) {
   };
   k.o1_groups = (k.NP + 3) / 4;
   split(k.Wd, (long long)((k.in_rows + 31) / 32) * k.o1_groups * k.B, k.o1_seg_x, k.o1_nseg_x);
-  int G = 1;
-  while ((k.NP + G - 1) / G > (G == 8 ? 5 : 4) && G < 8) G *= 2;
+  int G, npg;
+  o1_col_split(k.NP, G, npg);
   split(k.out_rows, (long long)((k.Wd + 32 / G - 1) / (32 / G)) * k.B, k.o1_seg_y, k.o1_nseg_y);
 }
 

@@ -88,6 +88,13 @@ struct O1Fit {
 };
 const O1Fit& o1_fit_cached(float sigma_s);
 
+// O(1) column pass: G lanes per column share the NP plane pairs, npg = ceil(NP / G) <= 7 each
+// (G = 1 up to 7 pairs: one lane holds every pair of its column, no cross-lane reduction).
+inline void o1_col_split(int NP, int& G, int& npg) {
+  G = NP <= 7 ? 1 : NP <= 14 ? 2 : NP <= 28 ? 4 : 8;
+  npg = (NP + G - 1) / G;
+}
+
 // Launch `kernel` on `s`; with pdl = true the launch carries the programmatic-stream-
 // serialization attribute (its prologue overlaps the previous kernel's tail; the kernel
 // calls pdl_wait() before consuming that kernel's output).

@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(32 * kO1Warps, 3) k_row_o1(const KParams p) {
 // ------------------------------------------------------------------ column pass + eqs. (8)-(10)
 
 constexpr int kO1D = 4;          // column pass: cp.async pipeline depth (rows in flight)
-constexpr int kO1ColNPGMax = 5;
+constexpr int kO1ColNPGMax = 7;
 
 struct ColO1Smem {
   float2 ring[kO1D][2][kO1ColNPGMax][32];   // [stage][enter/leave][pair][lane]
@@ -415,18 +415,24 @@ cudaError_t launch_col(const KParams& p, cudaStream_t s) {
   constexpr int CW = 32 / G;
   const long long nt = (long long)((p.Wd + CW - 1) / CW) * p.o1_nseg_y * p.B;
   const unsigned grid = (unsigned)((nt + kO1Warps - 1) / kO1Warps);
+  static bool attr = false;                        // > 48 KB dynamic shared memory: opt in once
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(k_col_o1<NPG, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)(kO1Warps * sizeof(ColO1Smem)));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
   return launch_k(k_col_o1<NPG, G>, dim3(grid), dim3(32 * kO1Warps), kO1Warps * sizeof(ColO1Smem), s,
                   p.ev[1] == nullptr, p);
 }
 
-template <int G>
+template <int G, int LO, int HI>
 cudaError_t launch_col_g(const KParams& p, int npg, cudaStream_t s) {
-  switch (npg) {
-    case 1: return launch_col<1, G>(p, s);
-    case 2: return launch_col<2, G>(p, s);
-    case 3: return launch_col<3, G>(p, s);
-    case 4: return launch_col<4, G>(p, s);
-    default: return launch_col<5, G>(p, s);
+  if constexpr (LO > HI) {
+    return cudaErrorInvalidValue;
+  } else {
+    if (npg <= LO) return launch_col<LO, G>(p, s);
+    return launch_col_g<G, LO + 1, HI>(p, npg, s);
   }
 }
 
@@ -448,15 +454,13 @@ cudaError_t launch_o1_two_pass(const KParams& p, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   if (p.ev[1]) cudaEventRecord(p.ev[1], s);
   // column pass: G lanes per column, NPG = ceil(NP / G) <= 5 pairs per lane
-  int G = 1;
-  while ((p.NP + G - 1) / G > (G == 8 ? 5 : 4) && G < 8) G *= 2;
-  const int npg = (p.NP + G - 1) / G;
-  if (npg > 5) return cudaErrorInvalidValue;
+  int G, npg;
+  o1_col_split(p.NP, G, npg);
   switch (G) {
-    case 1: e = launch_col_g<1>(p, npg, s); break;
-    case 2: e = launch_col_g<2>(p, npg, s); break;
-    case 4: e = launch_col_g<4>(p, npg, s); break;
-    default: e = launch_col_g<8>(p, npg, s); break;
+    case 1: e = launch_col_g<1, 1, 7>(p, npg, s); break;
+    case 2: e = launch_col_g<2, 4, 7>(p, npg, s); break;
+    case 4: e = launch_col_g<4, 4, 7>(p, npg, s); break;
+    default: e = launch_col_g<8, 4, 5>(p, npg, s); break;
   }
   if (p.ev[2]) cudaEventRecord(p.ev[2], s);
   return e;

@@ -5,6 +5,7 @@
 // arguments.  There is no CPU fallback: if the device path cannot run, the call fails
 // with a status code.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -162,6 +163,20 @@ void retain_pool() {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   done[dev] = true;
+}
+
+// Per-device copy-in / copy-out streams of gc_filter_host (created once, never destroyed).
+bool copy_streams(cudaStream_t* sin, cudaStream_t* sout) {
+  static std::mutex mu;
+  static cudaStream_t tab[64][2] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  for (int i = 0; i < 2; i++)
+    if (!tab[dev][i] && cudaStreamCreateWithFlags(&tab[dev][i], cudaStreamNonBlocking) != cudaSuccess) return false;
+  *sin = tab[dev][0];
+  *sout = tab[dev][1];
+  return true;
 }
 
 // Run the pipeline for the window described by k (rows/segments already set).
@@ -425,14 +440,78 @@ gc_status gc_filter_host(const float* imgs_host, int B, int H, int W, const gc_p
   if (e != cudaSuccess) return cuda_status(e);
   e = cudaMallocAsync((void**)&dout, bytes, s);
   if (e != cudaSuccess) { cudaFreeAsync(din, s); return cuda_status(e); }
-  e = cudaMemcpyAsync(din, imgs_host, bytes, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) {
-    st = gc_filter(din, B, H, W, p, dout, stream);
-    if (st == GC_OK) e = cudaMemcpyAsync(outs_host, dout, bytes, cudaMemcpyDeviceToHost, s);
+  // Pipeline: the input is copied in K chunks on a copy-in stream, each chunk is filtered on
+  // `s` as soon as the rows it reads have arrived, and copied back on a copy-out stream, so the
+  // two PCIe directions and the kernels overlap.  Chunks are images (B > 1) or row bands of one
+  // image (B = 1, gc_filter_window over the whole device image; halo rows come from the
+  // neighbouring chunks' copies).  Results are identical to gc_filter up to the O(1)
+  // operator's segment-dependent rounding (FIR: bit-identical).
+  const int R = radius_of(p->sigma_s);
+  // chunks of >= ~2 MB (smaller copies do not amortise their launch and event costs)
+  int K = (int)std::max<size_t>(1, std::min<size_t>(8, bytes / (2u << 20)));
+  if (B > 1) K = std::min(K, B);
+  else K = std::max(1, std::min(K, H / std::max(1, 8 * R)));
+  if (const char* env = std::getenv("GC_HOST_CHUNKS")) K = std::max(1, std::min(atoi(env), B > 1 ? B : H));
+  cudaStream_t sin = nullptr, sout = nullptr;
+  std::vector<cudaEvent_t> ev_in(K, nullptr), ev_comp(K, nullptr);
+  cudaEvent_t ev_start = nullptr, ev_done = nullptr;
+  bool ok = copy_streams(&sin, &sout) &&
+            cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) == cudaSuccess;
+  for (int k = 0; ok && k < K; k++)
+    ok = cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&ev_comp[k], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
+    st = GC_ECUDA;
+  } else {
+    // chunk k = [c0[k], c0[k+1]) images (B > 1) or rows (B = 1)
+    const int n = B > 1 ? B : H;
+    std::vector<int> c0(K + 1);
+    for (int k = 0; k <= K; k++) c0[k] = (int)((long long)n * k / K);
+    const size_t unit = B > 1 ? (size_t)H * W : (size_t)W;     // floats per image / per row
+    cudaEventRecord(ev_start, s);                                // device buffers allocated
+    cudaStreamWaitEvent(sin, ev_start, 0);
+    for (int k = 0; k < K && e == cudaSuccess; k++) {
+      const size_t off = (size_t)c0[k] * unit, cnt = (size_t)(c0[k + 1] - c0[k]) * unit;
+      e = cudaMemcpyAsync(din + off, imgs_host + off, cnt * 4, cudaMemcpyHostToDevice, sin);
+      if (e == cudaSuccess) e = cudaEventRecord(ev_in[k], sin);
+    }
+    for (int k = 0; k < K && e == cudaSuccess && st == GC_OK; k++) {
+      if (B > 1) {
+        cudaStreamWaitEvent(s, ev_in[k], 0);
+        st = gc_filter(din + (size_t)c0[k] * unit, c0[k + 1] - c0[k], H, W, p, dout + (size_t)c0[k] * unit, stream);
+      } else {
+        const int need = std::min(H - 1, c0[k + 1] - 1 + R);    // last input row the band reads
+        int j = k;
+        while (j + 1 < K && c0[j + 1] <= need) j++;
+        cudaStreamWaitEvent(s, ev_in[j], 0);                    // chunks 0..j have arrived
+        const float* seg[3] = {din, din, din};
+        const int seg_row0[3] = {0, -1, -1};
+        const int seg_rows[3] = {H, 0, 0};
+        st = gc_filter_window(seg, seg_row0, seg_rows, H, W, c0[k], c0[k + 1] - c0[k], p,
+                              dout + (size_t)c0[k] * unit, stream);
+      }
+      if (st == GC_OK) e = cudaEventRecord(ev_comp[k], s);
+    }
+    for (int k = 0; k < K && e == cudaSuccess && st == GC_OK; k++) {
+      const size_t off = (size_t)c0[k] * unit, cnt = (size_t)(c0[k + 1] - c0[k]) * unit;
+      cudaStreamWaitEvent(sout, ev_comp[k], 0);
+      e = cudaMemcpyAsync(outs_host + off, dout + off, cnt * 4, cudaMemcpyDeviceToHost, sout);
+    }
+    cudaEventRecord(ev_done, sout);
+    cudaEventRecord(ev_start, sin);
+    cudaStreamWaitEvent(s, ev_done, 0);                          // buffers free only after all
+    cudaStreamWaitEvent(s, ev_start, 0);                         // copies on both streams
   }
   cudaFreeAsync(din, s);
   cudaFreeAsync(dout, s);
   cudaError_t es = cudaStreamSynchronize(s);
+  for (int k = 0; k < K; k++) {
+    if (ev_in[k]) cudaEventDestroy(ev_in[k]);
+    if (ev_comp[k]) cudaEventDestroy(ev_comp[k]);
+  }
+  if (ev_start) cudaEventDestroy(ev_start);
+  if (ev_done) cudaEventDestroy(ev_done);
   if (st != GC_OK) return st;
   if (e != cudaSuccess) return cuda_status(e);
   return cuda_status(es);

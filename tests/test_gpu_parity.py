@@ -213,6 +213,29 @@ def test_filter_host_e2e(gc):
     assert np.array_equal(out, dev)
 
 
+@pytest.mark.parametrize("op", [1, 2])
+def test_filter_host_pipelined(gc, op):
+    """gc_filter_host splits large inputs into chunks (row bands of one image, or images of a
+    batch) whose copies overlap the kernels: identical to gc_filter for the FIR operator, to
+    rounding for the O(1) operator (segment-dependent fp32 order)."""
+    import torch
+    img = config_image("c2", H=1100, W=700)                      # 8 row bands at W_s = 15 / 30
+    s = 5.0 if op == 1 else 10.0
+    hin = torch.from_numpy(img).pin_memory()
+    out = gc.filter_host(hin.numpy(), s, 70.0, 8, op=op)
+    dev = gc.filter(torch.from_numpy(img).cuda(), s, 70.0, 8, op=op).cpu().numpy()
+    if op == 1:
+        assert np.array_equal(out, dev)
+    else:
+        assert np.max(np.abs(out - dev)) <= 1e-3
+    ref, _ = oracle.gc_filter_rows(img, [0, 137, 138, 550, 1099], s, 70.0, 8)
+    _gate(out[[0, 137, 138, 550, 1099]].astype(np.float64), ref, "filter_host bands")
+    imgs = np.stack([config_image("c4", index=i, H=300, W=310) for i in range(5)])
+    outb = gc.filter_host(imgs, 4.0, 85.0, 6, op=op)
+    devb = gc.filter(torch.from_numpy(imgs).cuda(), 4.0, 85.0, 6, op=op).cpu().numpy()
+    assert np.array_equal(outb, devb)
+
+
 def test_fallback_counter_and_stated_configs_reported(gc, capsys):
     """Stated (sigma_r, N): run and report (not gated, R1).  The guard of R8
     is exercised: guarded pixels are counted and pass f through."""

@@ -32,6 +32,10 @@
 //            G groups with shuffles; eq. (10) and the guard (R8) as in gc_fir.cu.
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "gc_device.cuh"
 
@@ -185,11 +189,13 @@ __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int
   }
   // ---- outputs x = xs .. xe-1, in chunks of 8 positions (xs is a multiple of 32)
   o1_stage_row(p, sm.fout, rowp, (xs - R) & ~(kO1CH - 1), lane, vec, p0);
-  const long long pstride = (long long)p.in_rows * p.Wd;
+  // O(1) plane layout [B][rows][NP][Wd]: the NP pairs of one image row are adjacent rows of
+  // a 2-D [B*rows*NP][Wd] tensor, so the column pass fetches a row's pairs with one TMA box
+  const long long rstride = (long long)p.NP * p.Wd;         // float2 between image rows
   const int orow = lane >> 3, ocol = lane & 7;
   const int rows_left = p.in_rows - (r0 + orow);            // rows r0+orow+4j valid for 4j < rows_left
-  float2* const obase = p.planes + b * p.planes_img_stride + (long long)p0 * pstride +
-                        (long long)(r0 + orow) * p.Wd + ocol;
+  float2* const obase = p.planes + b * p.planes_img_stride + (long long)(r0 + orow) * rstride +
+                        (long long)p0 * p.Wd + ocol;
 #pragma unroll 1
   for (int x = xs; x < xe; x += kO1OC) {
     const int nb = min(kO1OC, xe - x);
@@ -203,8 +209,8 @@ __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int
       for (int q = 0; q < NPG; q++) {
 #pragma unroll
         for (int j = 0; j < 8; j++)
-          if (4 * j < rows_left) o[(long long)(4 * j) * p.Wd] = sm.o[q][ocol][4 * j + orow];
-        o += pstride;
+          if (4 * j < rows_left) o[(long long)(4 * j) * rstride] = sm.o[q][ocol][4 * j + orow];
+        o += p.Wd;
       }
     }
     __syncwarp();
@@ -240,10 +246,40 @@ __global__ void __launch_bounds__(32 * kO1Warps, 3) k_row_o1(const KParams p) {
 constexpr int kO1D = 4;          // column pass: cp.async pipeline depth (rows in flight)
 constexpr int kO1ColNPGMax = 7;
 
-struct ColO1Smem {
+struct alignas(128) ColO1Smem {   // 128-byte aligned: TMA destinations
   float2 ring[kO1D][2][kO1ColNPGMax][32];   // [stage][enter/leave][pair][lane]
   float fring[kO1D][32];                    // f at the output row
+  unsigned long long full[kO1D];            // TMA mode: one mbarrier per stage
 };
+
+__device__ __forceinline__ void o1_mbar_init(unsigned long long* bar) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s));
+}
+__device__ __forceinline__ void o1_mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void o1_mbar_wait(unsigned long long* bar, unsigned phase) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(s),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void o1_tma_2d(void* smem, const CUtensorMap* map, int c0, int c1, unsigned long long* bar) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(s),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(b)
+      : "memory");
+}
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -257,10 +293,13 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int NPG, int G>
-__global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const KParams p) {
+// TMA = true (G = 1, NP <= NPG): each step's entering and leaving rows arrive as two 2-D TMA
+// boxes of [NP pairs][32 columns] (one elected lane, mbarrier per stage); otherwise per-lane
+// 8-byte cp.async copies.
+template <int NPG, int G, bool TMA>
+__global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const __grid_constant__ CUtensorMap tmap, const KParams p) {
   constexpr int CW = 32 / G;                       // columns per warp
-  extern __shared__ float4 smem_o1c[];
+  extern __shared__ __align__(1024) float4 smem_o1c[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   ColO1Smem& sm = reinterpret_cast<ColO1Smem*>(smem_o1c)[warp];
   const int ncb = (p.Wd + CW - 1) / CW;
@@ -278,8 +317,8 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const KParams p) {
   const int R = p.R;
   const int lead = 2 * R + 1;
   const int p0 = g * NPG;
-  const long long pstride = (long long)p.in_rows * p.Wd;
-  const float2* const src = p.planes + b * p.planes_img_stride + (long long)p0 * pstride + xc;
+  const long long rstride = (long long)p.NP * p.Wd;          // layout [B][rows][NP][Wd]
+  const float2* const src = p.planes + b * p.planes_img_stride + (long long)p0 * p.Wd + xc;
   int npl = p.NP - p0;                              // valid pairs of this lane's group
   npl = npl < 0 ? 0 : (npl > NPG ? NPG : npl);
 
@@ -302,6 +341,13 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const KParams p) {
     for (int q = 0; q < NPG; q++)
       if (q >= npl) sm.ring[st][0][q][lane] = sm.ring[st][1][q][lane] = make_float2(0.f, 0.f);
 
+  if (TMA) {
+    if (lane == 0) {
+      for (int st = 0; st < kO1D; st++) o1_mbar_init(&sm.full[st]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
   pdl_wait();                                       // planes from k_row_o1
   const bool fseg = p.seg[0].rows > 0 && p.out_row0 >= p.seg[0].row0 &&
                     p.out_row0 + p.out_rows <= p.seg[0].row0 + p.seg[0].rows;
@@ -309,14 +355,25 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const KParams p) {
                             (long long)(p.out_row0 - p.seg[0].row0) * p.Wd + xc;
   // step i (window centred on output-relative row i): entering row i+R+1, leaving row i-R
   auto issue = [&](int i, int st) {
-    const long long re = (long long)(mirror(p.out_row0 + i + R + 1, p.H) - p.in_row0) * p.Wd;
+    const int ye_row = mirror(p.out_row0 + i + R + 1, p.H) - p.in_row0;
     // (during the lead-in the leaving sample is masked to zero; read a valid row instead)
-    const long long rl = i >= ys ? (long long)(mirror(p.out_row0 + i - R, p.H) - p.in_row0) * p.Wd : re;
+    const int yl_row = i >= ys ? mirror(p.out_row0 + i - R, p.H) - p.in_row0 : ye_row;
+    if (TMA) {
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior reads of the stage
+        o1_mbar_expect_tx(&sm.full[st], 2u * p.NP * 32u * 8u);
+        const int x0 = cb * CW;
+        o1_tma_2d(&sm.ring[st][0][0][0], &tmap, x0, (b * p.in_rows + ye_row) * p.NP, &sm.full[st]);
+        o1_tma_2d(&sm.ring[st][1][0][0], &tmap, x0, (b * p.in_rows + yl_row) * p.NP, &sm.full[st]);
+      }
+    } else {
+      const long long re = (long long)ye_row * rstride, rl = (long long)yl_row * rstride;
 #pragma unroll
-    for (int q = 0; q < NPG; q++) {
-      if (q < npl) {
-        cp_async8(&sm.ring[st][0][q][lane], src + q * pstride + re);
-        cp_async8(&sm.ring[st][1][q][lane], src + q * pstride + rl);
+      for (int q = 0; q < NPG; q++) {
+        if (q < npl) {
+          cp_async8(&sm.ring[st][0][q][lane], src + q * p.Wd + re);
+          cp_async8(&sm.ring[st][1][q][lane], src + q * p.Wd + rl);
+        }
       }
     }
     const int fi = max(i, 0);
@@ -333,10 +390,12 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const KParams p) {
 #pragma unroll 1
   for (int i = i0; i < ye; i++) {
     const int k = i - i0;
+    if (TMA) __syncwarp();                          // all lanes are done with stage (k-1) % D
     if (i + kO1D - 1 < ye) issue(i + kO1D - 1, (k + kO1D - 1) % kO1D);
     cp_commit();
     cp_wait<kO1D - 1>();                            // this lane's copies for step i landed
     const int st = k % kO1D;
+    if (TMA) o1_mbar_wait(&sm.full[st], (k / kO1D) & 1);
     float2 pe[NPG], pl[NPG];
     const bool live = i >= ys;                      // lead-in: leaving samples are zero
 #pragma unroll
@@ -410,20 +469,44 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const KParams p) {
 
 namespace {
 
+// TMA descriptor of the O(1) plane buffer [B*rows*NP][Wd] (8-byte elements), box 32 x NP.
+bool make_o1_plane_map(CUtensorMap* map, const KParams& p) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)p.Wd, (cuuint64_t)p.B * p.in_rows * p.NP};
+  const cuuint64_t strides[1] = {(cuuint64_t)p.Wd * 8};
+  const cuuint32_t box[2] = {32, (cuuint32_t)p.NP};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_INT64, 2, (void*)p.planes, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int NPG, int G>
 cudaError_t launch_col(const KParams& p, cudaStream_t s) {
   constexpr int CW = 32 / G;
   const long long nt = (long long)((p.Wd + CW - 1) / CW) * p.o1_nseg_y * p.B;
   const unsigned grid = (unsigned)((nt + kO1Warps - 1) / kO1Warps);
-  static bool attr = false;                        // > 48 KB dynamic shared memory: opt in once
-  if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(k_col_o1<NPG, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  const bool tma = G == 1 && p.NP <= NPG && (p.Wd & 1) == 0 && make_o1_plane_map(&map, p);
+  auto kern = tma ? k_col_o1<NPG, G, true> : k_col_o1<NPG, G, false>;
+  static bool attr[2] = {false, false};            // > 48 KB dynamic shared memory: opt in once
+  if (!attr[tma]) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)(kO1Warps * sizeof(ColO1Smem)));
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[tma] = true;
   }
-  return launch_k(k_col_o1<NPG, G>, dim3(grid), dim3(32 * kO1Warps), kO1Warps * sizeof(ColO1Smem), s,
-                  p.ev[1] == nullptr, p);
+  return launch_k(kern, dim3(grid), dim3(32 * kO1Warps), kO1Warps * sizeof(ColO1Smem), s, p.ev[1] == nullptr,
+                  map, p);
 }
 
 template <int G, int LO, int HI>

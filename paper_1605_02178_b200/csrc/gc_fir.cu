@@ -239,7 +239,7 @@ __device__ __forceinline__ void tma_2d(void* smem, const CUtensorMap* map, int c
 }
 
 template <int W>
-__global__ void __launch_bounds__(32 * (kColConsumers + 1), 3)
+__global__ void __launch_bounds__(32 * (kColConsumers + 1), 4)
     k_col_t(const __grid_constant__ CUtensorMap tmap, const KParams p, unsigned* task_ctr) {
   using C = ColCfg<W>;
   constexpr int RY = C::RY;

@@ -16,6 +16,7 @@
 // indices (template radius W), so the FFMA count is exactly (2W+1) per output and plane.
 // Radii above kMaxTemplW use the runtime-W kernels at the end of the file.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 
@@ -538,15 +539,18 @@ cudaError_t launch_t(const KParams& p, cudaStream_t s) {
   const size_t smem_c = (size_t)CC::SMEM;
   auto kr = k_row_t<W>;
   auto kc = k_col_t<W>;
-  static int occ_r = 0, occ_c = 0;       // per instantiation, computed once
-  if (occ_r == 0) {
-    cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r);
-    cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_r, kr, 32 * kRowWarpsPerCta, smem_r);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, kc, 32 * (kColConsumers + 1), smem_c);
-    occ_r = std::max(occ_r, 1);
-    occ_c = std::max(occ_c, 1);
-  }
+  static std::atomic<unsigned long long> ready{0};   // per instantiation and device
+  static std::atomic<int> occ_c_s{1};
+  cudaError_t e0 = once_per_device(ready, [&]() {
+    cudaError_t e = cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c);
+    int oc = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, kc, 32 * (kColConsumers + 1), smem_c);
+    if (e == cudaSuccess) occ_c_s.store(std::max(oc, 1));
+    return e;
+  });
+  if (e0 != cudaSuccess) return e0;
+  const int occ_c = occ_c_s.load();
   CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
   if ((p.Wd & 1) == 0 && !make_plane_map(&map, p, CC::NJ)) return cudaErrorInvalidValue;
@@ -579,7 +583,11 @@ struct Table<0> {
 
 cudaError_t launch_rt(const KParams& p, cudaStream_t s) {
   const size_t smem = (size_t)4 * (64 + 2 * p.R) * 16;
-  cudaError_t e = cudaFuncSetAttribute(k_row_rt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static std::atomic<unsigned long long> ready{0};
+  cudaError_t e = once_per_device(ready, [&]() {   // the largest radius's size: covers every call
+    return cudaFuncSetAttribute(k_row_rt, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)((size_t)4 * (64 + 2 * kMaxFirW) * 16));
+  });
   if (e != cudaSuccess) return e;
   dim3 gr((p.Wd + 63) / 64, (p.in_rows + 3) / 4, p.B);
   if (p.ev[0]) cudaEventRecord(p.ev[0], s);

@@ -8,6 +8,8 @@
 // checked against the oracle element by element.  Plain one-thread-per-output kernels: FP64
 // runs at half the FP32 rate on B200 and this mode is a correctness instrument, not the
 // throughput path.
+#include <atomic>
+
 #include "gc_device.cuh"
 
 namespace gc {
@@ -118,7 +120,11 @@ __global__ void __launch_bounds__(256) k_col_f64(const KParams p) {
 
 cudaError_t launch_fp64_two_pass(const KParams& p, cudaStream_t s) {
   const size_t smem = (size_t)kF64TY * (kF64TX + 2 * p.R) * (sizeof(double2) + sizeof(double));
-  cudaError_t e = cudaFuncSetAttribute(k_row_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static std::atomic<unsigned long long> ready{0};
+  cudaError_t e = once_per_device(ready, [&]() {   // the largest radius's size: covers every call
+    return cudaFuncSetAttribute(k_row_f64, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)((size_t)kF64TY * (kF64TX + 2 * kMaxFirW) * (sizeof(double2) + sizeof(double))));
+  });
   if (e != cudaSuccess) return e;
   if (p.ev[0]) cudaEventRecord(p.ev[0], s);
   dim3 gr((p.Wd + kF64TX - 1) / kF64TX, (p.in_rows + kF64TY - 1) / kF64TY, p.B);

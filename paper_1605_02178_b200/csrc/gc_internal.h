@@ -2,6 +2,7 @@
 // kernels (gc_fir.cu).  Not part of the public ABI.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <utility>
 
@@ -93,6 +94,19 @@ const O1Fit& o1_fit_cached(float sigma_s);
 inline void o1_col_split(int NP, int& G, int& npg) {
   G = NP <= 7 ? 1 : NP <= 14 ? 2 : NP <= 28 ? 4 : 8;
   npg = (NP + G - 1) / G;
+}
+
+// Per-device one-time setup (function attributes are per device context): run fn once per
+// (call site, device); fn must be idempotent (two threads may both run it once).
+template <typename F>
+cudaError_t once_per_device(std::atomic<unsigned long long>& done, F&& fn) {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) return cudaErrorInvalidDevice;
+  const unsigned long long bit = 1ull << (d & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  const cudaError_t e = fn();
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
 }
 
 // Launch `kernel` on `s`; with pdl = true the launch carries the programmatic-stream-

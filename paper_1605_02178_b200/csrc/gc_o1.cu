@@ -31,6 +31,7 @@
 //            prefetched one step ahead; partial P', Q' of eqs. (8)-(9) are reduced across the
 //            G groups with shuffles; eq. (10) and the guard (R8) as in gc_fir.cu.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 
@@ -498,13 +499,11 @@ cudaError_t launch_col(const KParams& p, cudaStream_t s) {
   std::memset(&map, 0, sizeof(map));
   const bool tma = G == 1 && p.NP <= NPG && (p.Wd & 1) == 0 && make_o1_plane_map(&map, p);
   auto kern = tma ? k_col_o1<NPG, G, true> : k_col_o1<NPG, G, false>;
-  static bool attr[2] = {false, false};            // > 48 KB dynamic shared memory: opt in once
-  if (!attr[tma]) {
-    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)(kO1Warps * sizeof(ColO1Smem)));
-    if (e != cudaSuccess) return e;
-    attr[tma] = true;
-  }
+  static std::atomic<unsigned long long> ready[2];  // > 48 KB dynamic shared memory: opt in per device
+  const cudaError_t e = once_per_device(ready[tma], [&]() {
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kO1Warps * sizeof(ColO1Smem)));
+  });
+  if (e != cudaSuccess) return e;
   return launch_k(kern, dim3(grid), dim3(32 * kO1Warps), kO1Warps * sizeof(ColO1Smem), s, p.ev[1] == nullptr,
                   map, p);
 }
@@ -524,11 +523,12 @@ cudaError_t launch_col_g(const KParams& p, int npg, cudaStream_t s) {
 cudaError_t launch_o1_two_pass(const KParams& p, cudaStream_t s) {
   // row pass
   const size_t smem_r = (size_t)kO1Warps * sizeof(RowO1Smem);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_row_o1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r);
+  static std::atomic<unsigned long long> ready{0};
+  {
+    const cudaError_t e = once_per_device(ready, [&]() {
+      return cudaFuncSetAttribute(k_row_o1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r);
+    });
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const long long ntr = (long long)((p.in_rows + 31) / 32) * p.o1_nseg_x * p.o1_groups * p.B;
   if (p.ev[0]) cudaEventRecord(p.ev[0], s);

@@ -155,3 +155,40 @@ def test_band_path_single_rank_nccl(gc):
         assert torch.equal(band, whole)
     comm.close()
     dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,sigma_s", [("c5", 16.0), ("c3", 40.0)])
+def test_parity_full_size_sampled_rows_o1(gc, cfg, sigma_s):
+    """The O(1) path at BASELINE's full sizes in bench.py's launch configuration (c5 16384^2,
+    c3 4096^2 at sigma_s = 40), twin sigma_r: rows at both edges, at segment-sized strides and
+    in the middle, compared with the oracle evaluated at those rows."""
+    import torch
+    c = CONFIGS[cfg]
+    img = config_image(c)
+    t = torch.from_numpy(img).cuda()
+    out = gc.filter(t, sigma_s, c.sigma_r_twin, c.N)          # GC_OP_AUTO -> O(1) at these radii
+    torch.cuda.synchronize()
+    H = img.shape[0]
+    rows = [0, 1, 47, 48, H // 4 + 3, H // 2, H - 49, H - 2, H - 1]
+    o = out[rows].cpu().numpy().astype(np.float64)
+    del out, t
+    ref, nfb = oracle.gc_filter_rows(img, rows, sigma_s, c.sigma_r_twin, c.N)
+    assert nfb == 0
+    err = np.abs(o - ref)
+    assert err.max() <= MAX_ABS and math.sqrt(np.mean(err ** 2)) <= RMS, (err.max(), math.sqrt(np.mean(err ** 2)))
+
+
+@pytest.mark.parametrize("op", [OP_FIR, OP_O1])
+def test_maximum_degree_and_radius(gc, op):
+    """N = GC_N_MAX = 64 (33 plane pairs) and a radius at the FIR limit, W = 1023 (sigma_s = 341),
+    the latter on an image far smaller than the window (repeated reflections)."""
+    import torch
+    img = config_image("c2", H=70, W=90)
+    t = torch.from_numpy(img).cuda()
+    ref, _ = oracle.gc_filter(img, 4.0, 30.0, 64)
+    out = gc.filter(t, 4.0, 30.0, 64, op=op).cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(out - ref)) <= MAX_ABS
+    s = 341.0                                                   # W_s = 1023
+    ref, _ = oracle.gc_filter(img, s, 100.0, 5)
+    out = gc.filter(t, s, 100.0, 5, op=op).cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(out - ref)) <= MAX_ABS

@@ -13,6 +13,7 @@ sides read is `synth/` (seeded inputs, no method arithmetic).
 Modules
   chebyshev  eqs. (11)-(16), (18), (19), Taylor c_n        [pinned: tests/test_oracle_chebyshev.py]
   filters    eqs. (1), (6)-(10), (17), GCF pipeline         [pinned: tests/test_oracle_filters.py]
+  deriche    the Deriche-class recursive fast mode (NEXT-1)  [pinned: tests/test_oracle_deriche.py]
 
 Every function is pinned by at least one check that does not re-use its own
 formula (closed forms, library special cases, brute force, limits); see
@@ -42,4 +43,13 @@ from .filters import (  # noqa: F401
     psnr_db,
     rms,
     spatial_taps,
+)
+from .deriche import (  # noqa: F401
+    DERICHE,
+    deriche_2d,
+    deriche_coeffs,
+    deriche_filter_1d,
+    deriche_kernel,
+    deriche_pad,
+    gc_filter_deriche,
 )

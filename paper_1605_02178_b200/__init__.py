@@ -21,7 +21,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgc.so")
+LIB_PATH = os.environ.get("GC_LIB_PATH") or os.path.join(_HERE, "libgc.so")   # override: A/B timing of builds
 
 OP_AUTO, OP_FIR, OP_O1 = 0, 1, 2
 PREC_FP32, PREC_FP64 = 0, 1

@@ -93,6 +93,17 @@ __device__ __forceinline__ const float* row_ptr(const KParams& p, int b, int gy)
   return p.seg[0].ptr + b * p.seg_img_stride;  // unreachable after host validation
 }
 
+// Pointer to global row gy of image b if rows gy .. gy+n-1 all lie in one input segment
+// (consecutive rows then sit Wd floats apart), else nullptr.
+__device__ __forceinline__ const float* row_run_ptr(const KParams& p, int b, int gy, int n) {
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    const int r = gy - p.seg[k].row0;
+    if (r >= 0 && r + n <= p.seg[k].rows) return p.seg[k].ptr + b * p.seg_img_stride + (long long)r * p.Wd;
+  }
+  return nullptr;
+}
+
 // Eq. (17) centring and the scaled auxiliary variable a' = g / t_h in [-1, 1], plus the
 // Gaussian factor e = exp(-g^2 / 2 sigma_r^2) of eq. (6), as exp2(ex_k a'^2).
 __device__ __forceinline__ void centre(const KParams& p, float f, float& a, float& e) {

@@ -334,12 +334,12 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 4)
   unsigned nguard = 0;                             // guarded outputs of this lane (R8)
   float fo[RY], av[RY], P[RY], Q[RY], vpy[RY], pwx[RY], raw0[RY];
   int b = 0, x = 0, y0 = 0;
-  for (int k = 0;; k++) {
+  int pp = 0;                                      // stages arrive in (task, pair) order
+  for (int k = 0;; k++, pp = (pp + 1 == p.NP) ? 0 : pp + 1) {
     const int s = k % kColStages;
     mbar_wait(&full[s], (k / kColStages) & 1);
     const int task = stage_task[s];
     if (task < 0) break;
-    const int pp = k % p.NP;                       // stages arrive in (task, pair) order
     if (pp == 0) {
       const int rb = task % nrb;
       const int cb = (task / nrb) % ncb;
@@ -347,10 +347,17 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 4)
       y0 = rb * C::TROWS;
       x = cb * 32 + lane;
       // issue the loads of f now, use them after this pair's FIR (latency overlapped)
+      const int ya = y0 + RY * seg;
+      const float* run = ya + RY - 1 <= last ? row_run_ptr(p, b, p.out_row0 + ya, RY) : nullptr;
+      if (run) {
 #pragma unroll
-      for (int i = 0; i < RY; i++) {
-        const int yy = min(y0 + RY * seg + i, last);
-        fo[i] = (x < p.Wd) ? __ldg(row_ptr(p, b, p.out_row0 + yy) + x) : 0.f;
+        for (int i = 0; i < RY; i++) fo[i] = (x < p.Wd) ? __ldg(run + (long long)i * p.Wd + x) : 0.f;
+      } else {
+#pragma unroll
+        for (int i = 0; i < RY; i++) {
+          const int yy = min(ya + i, last);
+          fo[i] = (x < p.Wd) ? __ldg(row_ptr(p, b, p.out_row0 + yy) + x) : 0.f;
+        }
       }
     }
     const float2* col = sB + s * C::BUF + (RY * seg) * 32 + lane;
@@ -405,7 +412,7 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 4)
         if (p.raw) {
           o = raw0[i];
         } else if (Qi > 0.f && isfinite(Qi) && isfinite(Pi)) {
-          o = p.t_c + p.t_h * (Pi / Qi);                 // eq. (10) + uncentring
+          o = p.t_c + p.t_h * __fdividef(Pi, Qi);        // eq. (10) + uncentring
         } else {                                          // guard (R8)
           o = fminf(fmaxf(fo[i], p.L), p.U);
           nguard++;

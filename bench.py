@@ -35,6 +35,22 @@ METRIC = "megapixels/sec (fp32, degree N, σs) and % of HBM roofline at 1/2/4/8 
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.45: SMs x FP32 lanes x 2 x max SM clock
 
 
+def _hbm_peak():
+    """Measured HBM copy bandwidth (GB/s) from the driver-written MEASURED_PEAKS.json, else the
+    B200_PROFILING.md fallback."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        for k, v in d.items():
+            if "hbm" in k.lower() and isinstance(v, (int, float)) and v > 100:
+                return float(v)
+    except Exception:
+        pass
+    return 6550.7
+
+
+HBM_PEAK_GBPS = _hbm_peak()
+
+
 def _args():
     a = argparse.ArgumentParser()
     a.add_argument("--gpus", type=int, default=1)
@@ -47,7 +63,7 @@ def _args():
     a.add_argument("--no-e2e", action="store_true")
     a.add_argument("--batch", type=int, default=None, help="override the batch size (profiling only)")
     a.add_argument("--no-cpu-baseline", action="store_true")
-    a.add_argument("--op", type=int, default=0, choices=[0, 1, 2], help="0 auto, 1 FIR, 2 O(1)")
+    a.add_argument("--op", type=int, default=0, choices=[0, 1, 2, 3], help="0 auto, 1 FIR, 2 O(1), 3 Deriche (NOT eq. 7)")
     a.add_argument("--fp64", action="store_true", help="binary64 internal arithmetic (GC_PREC_FP64)")
     return a.parse_args()
 
@@ -65,14 +81,27 @@ O1_FLOP_PER_PLANE = 50   # exact-window recursion per plane-sample and pass (DES
 #                          A, B (2 add) + box (2 add, 1 mul) + 5 resonators x (3 FMA + 1 add + 1 FMA)
 
 
+DR_FLOP_PER_PLANE = 35  # Deriche mode per plane-sample and pass: 2 sections x 4 FMA per direction
+#                         (16 FMA = 32 FLOP) + 3 adds (section sums, causal + anticausal)
+
+
 def resolve_op(op, R):
     """GC_OP_AUTO -> FIR for W_s <= 16, O(1) above (include/gc.h, gc_api.cpp)."""
-    return op if op in (1, 2) else (2 if R >= 17 else 1)
+    return op if op in (1, 2, 3) else (2 if R >= 17 else 1)
 
 
 def op_flop_per_plane(op, R):
-    """Algorithmic FLOP of eq. (7) per plane-pixel and pass: FIR 2(2R+1); O(1) 50."""
-    return 2 * (2 * R + 1) if op == 1 else O1_FLOP_PER_PLANE
+    """Algorithmic FLOP of the spatial operator per plane-pixel and pass: FIR 2(2R+1); O(1) 50;
+    Deriche 35 (lead-in samples excluded)."""
+    return {1: 2 * (2 * R + 1), 2: O1_FLOP_PER_PLANE, 3: DR_FLOP_PER_PLANE}[op]
+
+
+def dr_bytes(N, px):
+    """Deriche mode, bytes per launch of its two-pass design (NP plane pairs):
+    k_row: f read by both sweeps (8) + causal sums written and re-read (16 NP) + planes written (8 NP);
+    k_col: planes read by both sweeps (16 NP) + causal sums written and re-read (16 NP) + f + out (8)."""
+    NP = (N + 3) // 2
+    return {"k_row": px * (8 + 24 * NP), "k_col": px * (8 + 32 * NP)}
 
 
 def flops_row(N, R, px, op=1):
@@ -336,6 +365,10 @@ def main():
                    "k_col": {"ms": col_ms, "tflops": fc / col_ms / 1e9}}
         dom = "k_col" if col_ms >= row_ms else "k_row"
         ach = kernels[dom]["tflops"]
+        if op == 3:                                # Deriche mode: HBM bytes of the design, too
+            db = dr_bytes(cfg.N, B * H * W)
+            for k, ms in (("k_row", row_ms), ("k_col", col_ms)):
+                kernels[k]["GBps"] = db[k] / ms / 1e6
         traffic = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
@@ -348,9 +381,13 @@ def main():
                 "frac": ach / FP32_PEAK_TFLOPS, "traffic": traffic,
                 "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP x 1.965 GHz (B200_PROFILING.md unit "
                                "counts; FFMA measured at 125-128 lanes/clk/SM, profiles/r01_ubench_fp32.txt)"}
+        if op == 3 and kernels[dom]["GBps"] / HBM_PEAK_GBPS > roof["frac"]:
+            roof = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["GBps"], "peak": HBM_PEAK_GBPS,
+                    "unit": "GB/s", "frac": kernels[dom]["GBps"] / HBM_PEAK_GBPS, "traffic": traffic,
+                    "peak_source": "MEASURED_PEAKS.json copy bandwidth (DESIGN.md §5.6 bytes per launch)"}
     ms_step = total_ms / K
     hbm = {"algorithmic_bytes_per_px": 8, "achieved_GBps": 8 * px_rank / (ms_step / 1e3) / 1e9}
-    hbm["frac_of_measured"] = hbm["achieved_GBps"] / 6550.7
+    hbm["frac_of_measured"] = hbm["achieved_GBps"] / HBM_PEAK_GBPS
     line = {"metric": METRIC, "value": value, "unit": "MP/s", "n_gpus": ws, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if cfg.name in ("c4", "c5") else "weak", "vs_baseline": None, "dtype": "f64" if args.fp64 else "f32",

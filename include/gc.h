@@ -55,15 +55,23 @@ typedef enum {
 #define GC_N_MAX 64          /* maximum polynomial degree N                           */
 #define GC_MU_MAX 4096.0     /* maximum mu = (U-L)^2 / (4 sigma_r^2) for gc_coeffs    */
 
-/* Spatial operator used for eq. (7).  Both compute the truncated sum over Omega exactly
-   as eq. (7) writes it (R3); they differ only in cost and rounding. */
+/* Spatial operator used for eq. (7).  FIR and O1 compute the truncated sum over Omega
+   exactly as eq. (7) writes it (R3); they differ only in cost and rounding.
+   DERICHE replaces it by the recursive filter the paper cites for its O(1) claim. */
 typedef enum {
   GC_OP_AUTO = 0,  /* library choice by W_s: FIR for W_s <= 16, O1 above  */
   GC_OP_FIR = 1,   /* direct separable FIR, 2(2W_s+1) FMA per plane-pixel; W_s <= 1024   */
-  GC_OP_O1 = 2     /* exact-window O(1) recursion: the truncated window of eq. (7) with
+  GC_OP_O1 = 2,    /* exact-window O(1) recursion: the truncated window of eq. (7) with
                       the taps replaced by a 6-term cosine least-squares fit (max error
                       ~1e-6 of the peak tap); 30 FMA-class ops per plane-pixel and pass,
                       independent of sigma_s; W_s <= 4096                                  */
+  GC_OP_DERICHE = 3 /* NOT eq. (7): the untruncated 4th-order recursive Gaussian of
+                      [Deriche1993] that P:50 / P:112 cite for the O(1) claim (SURVEY §8(f)
+                      NEXT-1): causal + anticausal recursions on each line padded with
+                      ceil(10 sigma_s) mirrored samples, zero initial state.  Opt-in only
+                      (GC_OP_AUTO never picks it); N <= 14; fp32 only; windows and bands
+                      need K = ceil(10 sigma_s) halo rows instead of W_s.  Moves the GCF by
+                      ~0.2-0.35 grey levels against eq. (7)                */
 } gc_operator;
 
 /* Human-readable name of a status code (static storage). */

@@ -17,13 +17,13 @@ import numpy as np
 __all__ = [
     "GCError", "lib", "coeffs", "bilateral", "bilateral_batch", "bilateral_c", "filter",
     "filter_host", "filter_window", "band_plan", "Comm", "bilateral_band", "version",
-    "OP_AUTO", "OP_FIR", "OP_O1", "gaussian", "operator_taps", "bilateral_direct",
+    "OP_AUTO", "OP_FIR", "OP_O1", "OP_DERICHE", "gaussian", "operator_taps", "bilateral_direct",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GC_LIB_PATH") or os.path.join(_HERE, "libgc.so")   # override: A/B timing of builds
 
-OP_AUTO, OP_FIR, OP_O1 = 0, 1, 2
+OP_AUTO, OP_FIR, OP_O1, OP_DERICHE = 0, 1, 2, 3   # gc_operator (include/gc.h)
 PREC_FP32, PREC_FP64 = 0, 1
 _STATUS = {0: "GC_OK", 1: "GC_EINVAL", 2: "GC_ERANGE", 3: "GC_ECUDA", 4: "GC_ENOMEM", 5: "GC_ENCCL"}
 

@@ -26,6 +26,12 @@ bool overlap(const void* a, size_t na, const void* b, size_t nb) {
 // W_s = ceil(3 sigma_s) (R4)
 int radius_of(float sigma_s) { return (int)std::ceil(3.0 * (double)sigma_s); }
 
+// Rows of input a window's output rows depend on, per side: W_s for eq. (7), the lead-in /
+// padding K = ceil(10 sigma_s) for the Deriche operator.
+int halo_of(const gc_params* p) {
+  return p->op == GC_OP_DERICHE ? (int)std::ceil(10.0 * (double)p->sigma_s) : radius_of(p->sigma_s);
+}
+
 // Truncated, normalised spatial taps k_m = exp(-m^2 / 2 sigma_s^2) / sum, |m| <= R (eq. 7).
 std::vector<double> taps_of(float sigma_s, int R) {
   std::vector<double> k(2 * R + 1);
@@ -74,8 +80,14 @@ gc_status validate_params(const gc_params* p) {
   if (p->N > GC_N_MAX) return GC_ERANGE;
   if (!finite_pos(p->sigma_s) || !finite_pos(p->sigma_r)) return GC_EINVAL;
   if (!std::isfinite(p->L) || !std::isfinite(p->U) || !(p->U > p->L)) return GC_EINVAL;
-  if (p->op != GC_OP_AUTO && p->op != GC_OP_FIR && p->op != GC_OP_O1) return GC_EINVAL;
+  if (p->op != GC_OP_AUTO && p->op != GC_OP_FIR && p->op != GC_OP_O1 && p->op != GC_OP_DERICHE) return GC_EINVAL;
   if (p->precision != GC_PREC_FP32 && p->precision != GC_PREC_FP64) return GC_EINVAL;
+  if (p->op == GC_OP_DERICHE) {
+    // recursive mode: fp32 only, all NP <= 8 plane pairs of a column held by one lane
+    if (p->precision != GC_PREC_FP32) return GC_EINVAL;
+    if ((p->N + 3) / 2 > kDrMaxPairs) return GC_ERANGE;
+    if (std::ceil(10.0 * (double)p->sigma_s) > (double)kO1MaxW) return GC_ERANGE;
+  }
   if (radius_of(p->sigma_s) > (p->op == GC_OP_FIR || p->precision == GC_PREC_FP64 ? kMaxFirW : kO1MaxW))
     return GC_ERANGE;
   if (p->c) {
@@ -139,6 +151,7 @@ gc_status fill_constants(const gc_params* p, KParams& k, std::vector<float2>& ta
   if (k.fp64) op = GC_OP_FIR;                     // binary64 mode: the exact FIR of eq. (7)
   k.op = op;
   if (op == GC_OP_O1) o1_constants(p->sigma_s, k);
+  if (op == GC_OP_DERICHE) deriche_constants(p->sigma_s, k);
   return GC_OK;
 }
 
@@ -146,6 +159,22 @@ gc_status cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return GC_OK;
   if (e == cudaErrorMemoryAllocation) return GC_ENOMEM;
   return GC_ECUDA;
+}
+
+// Segment lengths of the Deriche passes (gc_deriche.cu): ~16 warps per SM where the image
+// allows, segments no shorter than two lead-ins (K = ceil(10 sigma_s) samples each);
+// row-pass segments are multiples of 8 columns (shared-memory store chunks).
+void dr_segments(KParams& k) {
+  const int target = k.num_sms * 16;
+  auto split = [&](int len, long long base, int align, int& seg, int& nseg) {
+    long long want = (target + base - 1) / base;
+    long long cap = std::max(1, len / (2 * k.dr_K));
+    int n = (int)std::max(1LL, std::min(want, cap));
+    seg = ((len + n - 1) / n + align - 1) / align * align;
+    nseg = (len + seg - 1) / seg;
+  };
+  split(k.Wd, (long long)((k.in_rows + 31) / 32) * k.B, 8, k.dr_seg_x, k.dr_nseg_x);
+  split(k.out_rows, (long long)((k.Wd + 31) / 32) * k.B, 1, k.dr_seg_y, k.dr_nseg_y);
 }
 
 // Keep freed stream-ordered scratch in the device's default pool instead of returning it
@@ -188,14 +217,18 @@ gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) 
   cudaDeviceGetAttribute(&k.num_sms, cudaDevAttrMultiProcessorCount, dev);
   const int op = k.op;
   if (op == GC_OP_O1) o1_segments(k);
+  if (op == GC_OP_DERICHE) dr_segments(k);
   const size_t plane_elems = (size_t)k.NP * k.in_rows * k.Wd;
   float2* planes = nullptr;
   float2* taps_dev = nullptr;
   // plane buffer + 256 bytes of task counters at its end
   const size_t elem = k.fp64 ? sizeof(double2) : sizeof(float2);
-  cudaError_t e = cudaMallocAsync((void**)&planes, plane_elems * k.B * elem + 256, s);
+  // (Deriche mode: a second plane-sized buffer after the counters for the causal partial sums)
+  const size_t scratch_elems = op == GC_OP_DERICHE ? plane_elems * k.B : 0;
+  cudaError_t e = cudaMallocAsync((void**)&planes, plane_elems * k.B * elem + 256 + scratch_elems * elem, s);
   if (e != cudaSuccess) return cuda_status(e);
   k.counters = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(planes) + plane_elems * k.B * elem);
+  k.scratch = scratch_elems ? reinterpret_cast<float2*>(reinterpret_cast<char*>(k.counters) + 256) : nullptr;
   if (k.fp64 || (op == GC_OP_FIR && k.R > kMaxTemplW)) {
     // taps for the runtime-radius kernels: (k_m, k_m) fp32 pairs, or k_m in binary64
     std::vector<double> td;
@@ -219,7 +252,10 @@ gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) 
   k.planes_img_stride = (long long)plane_elems;
   k.taps_g = taps_dev;
   k.taps_d = reinterpret_cast<const double*>(taps_dev);
-  e = k.fp64 ? launch_fp64_two_pass(k, s) : op == GC_OP_O1 ? launch_o1_two_pass(k, s) : launch_fir_two_pass(k, s);
+  e = k.fp64                ? launch_fp64_two_pass(k, s)
+      : op == GC_OP_O1      ? launch_o1_two_pass(k, s)
+      : op == GC_OP_DERICHE ? launch_deriche_two_pass(k, s)
+                            : launch_fir_two_pass(k, s);
   cudaError_t e2 = cudaFreeAsync(planes, s);
   if (taps_dev) cudaFreeAsync(taps_dev, s);
   if (e != cudaSuccess) return cuda_status(e);
@@ -279,7 +315,7 @@ gc_status gc_filter_window(const float* const seg[3], const int seg_row0[3], con
     nseg++;
   }
   if (nseg == 0) return GC_EINVAL;
-  const int R = radius_of(p->sigma_s);
+  const int R = halo_of(p);
   // rows the window needs (after symmetric extension) must all be in some segment
   int lo = H_global, hi = -1;
   auto mir = [&](int q) {
@@ -446,7 +482,7 @@ gc_status gc_filter_host(const float* imgs_host, int B, int H, int W, const gc_p
   // image (B = 1, gc_filter_window over the whole device image; halo rows come from the
   // neighbouring chunks' copies).  Results are identical to gc_filter up to the O(1)
   // operator's segment-dependent rounding (FIR: bit-identical).
-  const int R = radius_of(p->sigma_s);
+  const int R = halo_of(p);
   // chunks of >= ~2 MB (smaller copies do not amortise their launch and event costs)
   int K = (int)std::max<size_t>(1, std::min<size_t>(8, bytes / (2u << 20)));
   if (B > 1) K = std::min(K, B);

@@ -71,7 +71,8 @@ gc_status gc_bilateral_band(const float* band, int H_band, int W, int H_global, 
   ncclComm_t c = reinterpret_cast<ncclComm_t>(comm);
   int rank = 0, world = 1;
   if (ncclCommUserRank(c, &rank) != ncclSuccess || ncclCommCount(c, &world) != ncclSuccess) return GC_ENCCL;
-  const int R = (int)std::ceil(3.0 * (double)p->sigma_s);
+  // halo rows: W_s for eq. (7); the Deriche operator's lead-in K = ceil(10 sigma_s) for GC_OP_DERICHE
+  const int R = (int)std::ceil((p->op == GC_OP_DERICHE ? 10.0 : 3.0) * (double)p->sigma_s);
   const bool has_top = rank > 0, has_bot = rank < world - 1;
   if ((has_top || has_bot) && H_band <= R) return GC_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

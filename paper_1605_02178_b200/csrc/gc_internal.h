@@ -69,6 +69,13 @@ struct KParams {
   int o1_seg_y, o1_nseg_y;         // column pass: y-segment length and count
   int o1_groups;                   // row pass: plane-pair groups (<= 4 pairs each)
   int raw;                         // 1: eq. (7) of f itself (gc_gaussian): pair 0 = (f, 0), out = Fbar_0
+  // Deriche-class recursive operator (gc_deriche.cu; GC_OP_DERICHE): two 2nd-order sections per
+  // direction, 1/Z folded into b0, b1, c1, c2
+  float dr_b0[2], dr_b1[2], dr_c1[2], dr_c2[2], dr_a1[2], dr_a2[2];
+  int dr_K;                        // mirror padding / lead-in per side: ceil(10 sigma_s)
+  int dr_seg_x, dr_nseg_x;         // row pass: x-segment length (multiple of 8) and count
+  int dr_seg_y, dr_nseg_y;         // column pass: y-segment length and count
+  float2* scratch;                 // causal partial sums (as large as the plane buffer)
   // binary64 internal arithmetic (gc_fp64.cu; gc_params.precision = GC_PREC_FP64)
   int fp64;
   float sigma_s_host;                             // sigma_s (host side: taps)
@@ -134,6 +141,11 @@ cudaError_t launch_fir_two_pass(const KParams& p, cudaStream_t stream);
 
 // Launch the two-pass O(1) exact-window pipeline (gc_o1.cu).  Same buffers and semantics.
 cudaError_t launch_o1_two_pass(const KParams& p, cudaStream_t stream);
+
+// Two-pass Deriche-class recursive pipeline (gc_deriche.cu), NP <= kDrMaxPairs; p.scratch set.
+constexpr int kDrMaxPairs = 8;
+void deriche_constants(float sigma_s, KParams& k);
+cudaError_t launch_deriche_two_pass(const KParams& p, cudaStream_t stream);
 
 // Two-pass FIR pipeline in binary64 (gc_fp64.cu): planes are double2 pairs (twice the bytes).
 cudaError_t launch_fp64_two_pass(const KParams& p, cudaStream_t stream);

@@ -99,6 +99,16 @@ def test_device_entry_points_validate_before_cuda(gc):
     assert lib.gc_bilateral_direct(None, 1, 8, 8, 2.0, 30.0, fake2, None) == 1
     assert lib.gc_bilateral_direct(fake, 1, 8, 8, 2.0, 0.0, fake2, None) == 1
     assert lib.gc_bilateral_direct(fake, 1, 8, 8, 500.0, 30.0, fake2, None) == 2  # W_s > 1024
+    # Deriche operator (GC_OP_DERICHE = 3): N <= 14, fp32 only; validated before CUDA
+    p = gc._Params()
+    lib.gc_params_init(ctypes.byref(p), 15, 3.0, 30.0)
+    p.op = 3
+    assert lib.gc_filter(fake, 1, 8, 8, ctypes.byref(p), fake2, None) == 2       # NP = 9 > 8
+    p.N, p.precision = 12, 1
+    assert lib.gc_filter(fake, 1, 8, 8, ctypes.byref(p), fake2, None) == 1       # binary64 + Deriche
+    p.precision, p.op = 0, 4
+    assert lib.gc_filter(fake, 1, 8, 8, ctypes.byref(p), fake2, None) == 1       # unknown operator
+    assert lib.gc_operator_taps(3.0, 3, None, None) == 1                           # IIR: no finite taps
 
 
 def test_status_strings(gc):

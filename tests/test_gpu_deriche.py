@@ -1,0 +1,137 @@
+"""GPU tests of the Deriche-class recursive fast mode (GC_OP_DERICHE)
+against its binary64 oracle (oracle/deriche.py: the 4th-order recursions of [Deriche1993],
+which P:50 / P:112 cite for the O(1) claim, on K = ceil(10 s) mirror-padded lines).
+
+The GPU runs the same transfer function as two 2nd-order sections per direction in fp32,
+on line segments that start from zero state K samples before / after their outputs (the
+oracle starts at the padded edge): the two differ by rounding (~1e-5 relative at s = 40)
+and by the |q|^K ~ 3e-8 start-up transient.  The GCF is gated at the north star's
+tolerances (max-abs 1e-2, RMS 1e-3) at the sigma_r twins (R1)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import deriche as D
+from synth import CONFIGS, config_image
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS, RMS = 1e-2, 1e-3
+OP_DERICHE = 3
+
+
+@pytest.fixture(scope="module")
+def gc(cuda_device):
+    import paper_1605_02178_b200 as gc
+    return gc
+
+
+def _gauss(gc, img, sigma_s):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(img, dtype=np.float32)).cuda()
+    out = gc.gaussian(t, sigma_s, op=OP_DERICHE)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("sigma_s", [1.5, 5.0, 16.0])
+def test_impulse_response_is_the_closed_form(gc, sigma_s):
+    """A unit impulse far from the edges returns h(|m|) h(|n|) / Z^2 (the closed form of the
+    4th-order fit, oracle.deriche.deriche_kernel), i.e. the operator is separable, symmetric
+    and normalised, with no truncation at 3 sigma_s."""
+    K = math.ceil(10 * sigma_s)
+    n = 2 * K + 23
+    img = np.zeros((n, n + 5), np.float32)
+    cy, cx = n // 2, (n + 5) // 2
+    img[cy, cx] = 1.0
+    out = _gauss(gc, img, sigma_s)
+    _, _, _, Z = D.deriche_coeffs(sigma_s)
+    hy = D.deriche_kernel(np.arange(n) - cy, sigma_s) / Z
+    hx = D.deriche_kernel(np.arange(n + 5) - cx, sigma_s) / Z
+    ref = np.outer(hy, hx)
+    assert np.max(np.abs(out - ref)) <= 2e-5 * ref.max()
+    assert abs(out.sum() - 1.0) <= 1e-4
+
+
+@pytest.mark.parametrize("sigma_s,H,W", [(1.0, 33, 47), (3.0, 256, 256), (5.0, 131, 300), (5.0, 1024, 1024),
+                                         (16.0, 300, 290), (16.0, 700, 1030), (40.0, 130, 170),
+                                         (3.0, 1, 50), (4.0, 37, 1), (12.0, 5, 9), (2.0, 1, 1)])
+def test_gaussian_vs_oracle(gc, sigma_s, H, W):
+    """The operator alone on a config-like 0-255 image, ragged sizes, several segments per
+    line, lines shorter than the padding (repeated reflections), 1x1."""
+    img = config_image("c2", H=max(H, 2), W=max(W, 2))[:H, :W].astype(np.float64)
+    out = _gauss(gc, img, sigma_s)
+    ref = D.deriche_2d(img, sigma_s)
+    tol = 255 * (2e-5 if sigma_s < 20 else 6e-5)
+    assert np.max(np.abs(out - ref)) <= tol, np.max(np.abs(out - ref))
+
+
+@pytest.mark.parametrize("cfg,sigma_s,H,W", [
+    ("c1", 3.0, 256, 256),
+    ("c2", 5.0, 300, 280),
+    ("c3", 10.0, 200, 333),
+    ("c4", 4.0, 129, 260),
+    ("c5", 16.0, 352, 400),
+])
+def test_gcf_parity_twin(gc, cfg, sigma_s, H, W):
+    """GCF with the Deriche operator vs oracle.gc_filter_deriche at the sigma_r twins."""
+    import torch
+    c = CONFIGS[cfg]
+    img = config_image(c, H=H, W=W)
+    t = torch.from_numpy(img).cuda()
+    out = gc.filter(t, sigma_s, c.sigma_r_twin, c.N, op=OP_DERICHE)
+    torch.cuda.synchronize()
+    out = out.cpu().numpy().astype(np.float64)
+    ref, nfb = D.gc_filter_deriche(img, sigma_s, c.sigma_r_twin, c.N)
+    assert nfb == 0
+    err = np.abs(out - ref)
+    ma, rms = float(err.max()), float(math.sqrt(np.mean(err ** 2)))
+    assert ma <= MAX_ABS and rms <= RMS, f"{cfg} sigma_s={sigma_s} {H}x{W}: max-abs {ma:.3e} rms {rms:.3e}"
+
+
+def test_gcf_batch_and_constant_image(gc):
+    """A batch [B][H][W] equals per-image calls; a constant image is returned unchanged
+    (P/Q = sigma_r a for Q > 0) by the recursive operator too."""
+    import torch
+    c = CONFIGS["c4"]
+    imgs = np.stack([config_image(c, index=i, H=70, W=90) for i in range(3)] + [np.full((70, 90), 77.0, np.float32)])
+    t = torch.from_numpy(imgs).cuda()
+    out = gc.filter(t, 4.0, c.sigma_r_twin, c.N, op=OP_DERICHE).cpu().numpy()
+    for i in range(4):
+        one = gc.filter(t[i].contiguous(), 4.0, c.sigma_r_twin, c.N, op=OP_DERICHE).cpu().numpy()
+        assert np.array_equal(out[i], one)
+    assert np.max(np.abs(out[3] - 77.0)) <= 1e-3
+
+
+def test_virtual_bands_match_whole_image(gc):
+    """gc_filter_window over three row bands (halos of K = ceil(10 s) rows) reproduces the
+    whole-image result up to the segment-dependent start-up transient."""
+    import torch
+    c = CONFIGS["c5"]
+    img = config_image(c, H=420, W=300)
+    t = torch.from_numpy(img).cuda()
+    whole = gc.filter(t, 6.0, c.sigma_r_twin, c.N, op=OP_DERICHE).cpu().numpy().astype(np.float64)
+    K = math.ceil(60.0)
+    parts = []
+    for r0, r1 in [(0, 140), (140, 300), (300, 420)]:
+        a, b = max(0, r0 - K), min(420, r1 + K)
+        seg = [(t[a:b].contiguous(), a)]
+        parts.append(gc.filter_window(seg, 420, r0, r1 - r0, 6.0, c.sigma_r_twin, c.N, op=OP_DERICHE)
+                     .cpu().numpy().astype(np.float64))
+    got = np.concatenate(parts)
+    assert np.max(np.abs(got - whole)) <= 1e-3
+
+
+def test_deriche_is_not_eq7(gc):
+    """The documented gap: the recursive operator moves the GCF by more than the parity
+    tolerance against eq. (7) (0.2-0.35 grey levels), so GC_OP_AUTO never picks
+    it and it is compared with its own oracle only."""
+    import torch
+    c = CONFIGS["c2"]
+    img = config_image(c, H=200, W=190)
+    t = torch.from_numpy(img).cuda()
+    dr = gc.filter(t, 5.0, c.sigma_r_twin, c.N, op=OP_DERICHE).cpu().numpy().astype(np.float64)
+    ref, _ = oracle.gc_filter(img, 5.0, c.sigma_r_twin, c.N)
+    assert np.max(np.abs(dr - ref)) > 0.05

@@ -170,49 +170,93 @@ __global__ void __launch_bounds__(32 * kDrWarps) k_row_dr(const KParams p) {
   float2* const yp = p.scratch + (long long)b * p.NP * n * p.in_rows + rowc;
   const long long yp_pair = (long long)n * p.in_rows;
 
-  // ---- causal sweep, padded coordinates c in [max(x0 - K, -K), x1)
+  // f of this lane's row, 8 consecutive padded positions at a time (the next group's loads are
+  // issued before the current group's recursions)
+  auto load8 = [&](int c, float (&v)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) v[i] = __ldg(src + mirror(c + i, n));
+  };
+
+  // ---- causal sweep, padded coordinates c in [cs0, x1), cs0 = max(x0 - K, -K)
   DrCausal cs[NPG];
 #pragma unroll
   for (int q = 0; q < NPG; q++) cs[q].zero();
+  {
+    const int cs0 = max(x0 - K, -K);
+    float fc[8], fn[8];
+    load8(cs0, fn);
 #pragma unroll 1
-  for (int c = max(x0 - K, -K); c < x1; c++) {
-    float2 psi[NPG];
-    dr_planes<NPG>(p, __ldg(src + mirror(c, n)), psi);
+    for (int c8 = cs0; c8 < x1; c8 += 8) {
 #pragma unroll
-    for (int q = 0; q < NPG; q++) {
-      const float2 y = cs[q].step(p, psi[q]);
-      if (c >= x0 && q < p.NP && rok) yp[q * yp_pair + (long long)c * p.in_rows] = y;
+      for (int i = 0; i < 8; i++) fc[i] = fn[i];
+      if (c8 + 8 < x1) load8(c8 + 8, fn);
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const int c = c8 + i;
+        if (c >= x1) break;
+        float2 psi[NPG];
+        dr_planes<NPG>(p, fc[i], psi);
+#pragma unroll
+        for (int q = 0; q < NPG; q++) {
+          const float2 y = cs[q].step(p, psi[q]);
+          if (c >= x0 && rok) yp[q * yp_pair + (long long)c * p.in_rows] = y;
+        }
+      }
     }
   }
-  __syncwarp();   // (own stores re-read below: same thread, program order suffices)
 
-  // ---- anticausal sweep, c from min(x1 + K, n + K) - 1 down to x0; outputs in 8-column chunks
+  // ---- anticausal sweep, c from min(x1 + K, n + K) - 1 down to x0: lead-in, then the outputs
+  //      in 8-column chunks (f for the next 8 positions and the causal sums for the next
+  //      position prefetched)
   DrAnti as[NPG];
 #pragma unroll
   for (int q = 0; q < NPG; q++) as[q].zero();
   const int cstart = min(x1 + K, n + K) - 1;
+  {
+    float fc[8], fn[8];
+    if (cstart >= x1) load8(cstart - 7, fn);
 #pragma unroll 1
-  for (int c = cstart; c >= x1; c--) {   // lead-in: no outputs
-    float2 psi[NPG];
-    dr_planes<NPG>(p, __ldg(src + mirror(c, n)), psi);
+    for (int c8 = cstart; c8 >= x1; c8 -= 8) {   // positions c8, c8-1, .., c8-7 (>= x1)
 #pragma unroll
-    for (int q = 0; q < NPG; q++) as[q].step(p, psi[q]);
+      for (int i = 0; i < 8; i++) fc[i] = fn[i];
+      if (c8 - 8 >= x1) load8(c8 - 15, fn);
+#pragma unroll
+      for (int i = 7; i >= 0; i--) {
+        const int c = c8 - 7 + i;
+        if (c < x1) break;
+        float2 psi[NPG];
+        dr_planes<NPG>(p, fc[i], psi);
+#pragma unroll
+        for (int q = 0; q < NPG; q++) as[q].step(p, psi[q]);
+      }
+    }
   }
   float2* const dst = p.planes + b * p.planes_img_stride;
   const long long pstride = (long long)p.in_rows * n;
   const int nchunk = (x1 - x0 + kDrChunk - 1) / kDrChunk;
+  float2 ypn[NPG];
+#pragma unroll
+  for (int q = 0; q < NPG; q++) ypn[q] = yp[q * yp_pair + (long long)(x1 - 1) * p.in_rows];
 #pragma unroll 1
   for (int ch = nchunk - 1; ch >= 0; ch--) {
     const int c0 = x0 + ch * kDrChunk, c1 = min(c0 + kDrChunk, x1);
-#pragma unroll 1
-    for (int c = c1 - 1; c >= c0; c--) {
-      float2 psi[NPG];
-      dr_planes<NPG>(p, __ldg(src + mirror(c, n)), psi);
+    float fc[8];
+    load8(c0, fc);
 #pragma unroll
-      for (int q = 0; q < NPG; q++) {
-        const float2 w = as[q].step(p, psi[q]);
-        if (q < p.NP) sm.tile[q][lane][c - c0] = f2add(w, yp[q * yp_pair + (long long)c * p.in_rows]);
+    for (int i = kDrChunk - 1; i >= 0; i--) {
+      const int c = c0 + i;
+      if (c >= c1) continue;
+      float2 ypc[NPG];
+#pragma unroll
+      for (int q = 0; q < NPG; q++) ypc[q] = ypn[q];
+      if (c > x0) {
+#pragma unroll
+        for (int q = 0; q < NPG; q++) ypn[q] = yp[q * yp_pair + (long long)(c - 1) * p.in_rows];
       }
+      float2 psi[NPG];
+      dr_planes<NPG>(p, fc[i], psi);
+#pragma unroll
+      for (int q = 0; q < NPG; q++) sm.tile[q][lane][i] = f2add(as[q].step(p, psi[q]), ypc[q]);
     }
     __syncwarp();
     // rows of the chunk: lane -> (row r = lane / 8 + 4 i, column j = lane % 8)
@@ -268,7 +312,7 @@ __global__ void __launch_bounds__(32 * kDrWarps) k_col_dr(const KParams p) {
     const int gs = max(g0 - K, -K);
     float2 nx[NPG];
 #pragma unroll
-    for (int q = 0; q < NPG; q++) nx[q] = q < p.NP ? __ldg(pl + q * pstride + prow(gs)) : make_float2(0.f, 0.f);
+    for (int q = 0; q < NPG; q++) nx[q] = __ldg(pl + q * pstride + prow(gs));
 #pragma unroll 1
     for (int g = gs; g < g1; g++) {
       float2 cx[NPG];
@@ -277,59 +321,67 @@ __global__ void __launch_bounds__(32 * kDrWarps) k_col_dr(const KParams p) {
       if (g + 1 < g1) {
         const long long o = prow(g + 1);
 #pragma unroll
-        for (int q = 0; q < NPG; q++) nx[q] = q < p.NP ? __ldg(pl + q * pstride + o) : make_float2(0.f, 0.f);
+        for (int q = 0; q < NPG; q++) nx[q] = __ldg(pl + q * pstride + o);
       }
 #pragma unroll
       for (int q = 0; q < NPG; q++) {
         const float2 y = cs[q].step(p, cx[q]);
-        if (g >= g0 && q < p.NP) ys[q * ys_pair + (long long)(g - p.out_row0) * p.Wd] = y;
+        if (g >= g0) ys[q * ys_pair + (long long)(g - p.out_row0) * p.Wd] = y;
       }
     }
   }
 
   // ---- anticausal sweep up from min(g1 + K, H + K) - 1; outputs for g in [g0, g1)
+  //      (the plane row, causal sums and f of the next row are loaded one step ahead)
   DrAnti as[NPG];
 #pragma unroll
   for (int q = 0; q < NPG; q++) as[q].zero();
   unsigned nguard = 0;
   const int ge = min(g1 + K, H + K) - 1;
-  float2 nx[NPG];
+  float2 nx[NPG], ny[NPG];
+  float nf = 0.f;
+  auto fetch = [&](int g) {
+    const long long o = prow(g);
 #pragma unroll
-  for (int q = 0; q < NPG; q++) nx[q] = q < p.NP ? __ldg(pl + q * pstride + prow(ge)) : make_float2(0.f, 0.f);
+    for (int q = 0; q < NPG; q++) nx[q] = __ldg(pl + q * pstride + o);
+    if (g < g1) {
+      const long long oy = (long long)(g - p.out_row0) * p.Wd;
+#pragma unroll
+      for (int q = 0; q < NPG; q++) ny[q] = ys[q * ys_pair + oy];
+      nf = __ldg(row_ptr(p, b, g) + xc);
+    }
+  };
+  fetch(ge);
 #pragma unroll 1
   for (int g = ge; g >= g0; g--) {
-    float2 cx[NPG];
+    float2 cx[NPG], cy[NPG];
 #pragma unroll
-    for (int q = 0; q < NPG; q++) cx[q] = nx[q];
-    if (g - 1 >= g0) {
-      const long long o = prow(g - 1);
-#pragma unroll
-      for (int q = 0; q < NPG; q++) nx[q] = q < p.NP ? __ldg(pl + q * pstride + o) : make_float2(0.f, 0.f);
+    for (int q = 0; q < NPG; q++) {
+      cx[q] = nx[q];
+      cy[q] = ny[q];
     }
+    const float fo = nf;
+    if (g - 1 >= g0) fetch(g - 1);
     if (g >= g1) {
 #pragma unroll
       for (int q = 0; q < NPG; q++) as[q].step(p, cx[q]);
       continue;
     }
     const int yo = g - p.out_row0;
-    const float fo = __ldg(row_ptr(p, b, g) + xc);
     const float a = p.raw ? 0.f : centre_a(p, fo);
     const float2 a2 = f2s(a * a);
     float2 pw = make_float2(1.f, a), P2 = make_float2(0.f, 0.f), Q2 = make_float2(0.f, 0.f);
     float vpy = 0.f, raw0 = 0.f;
 #pragma unroll
     for (int q = 0; q < NPG; q++) {
-      const float2 w = as[q].step(p, cx[q]);
-      if (q < p.NP) {
-        const float2 F = f2add(w, ys[q * ys_pair + (long long)yo * p.Wd]);   // Fbar'_{2q}, Fbar'_{2q+1}
-        if (q == 0) raw0 = F.x;
-        // eqs. (8)-(9): Q += chat_n a'^n Fbar_n, P += chat_n a'^n Fbar_{n+1}
-        const float2 v2 = f2mul(p.chat2[q], pw);
-        Q2 = f2fma(v2, F, Q2);
-        P2 = f2fma(make_float2(vpy, v2.x), F, P2);
-        vpy = v2.y;
-        pw = f2mul(pw, a2);
-      }
+      const float2 F = f2add(as[q].step(p, cx[q]), cy[q]);   // Fbar'_{2q}, Fbar'_{2q+1}
+      if (q == 0) raw0 = F.x;
+      // eqs. (8)-(9): Q += chat_n a'^n Fbar_n, P += chat_n a'^n Fbar_{n+1}
+      const float2 v2 = f2mul(p.chat2[q], pw);
+      Q2 = f2fma(v2, F, Q2);
+      P2 = f2fma(make_float2(vpy, v2.x), F, P2);
+      vpy = v2.y;
+      pw = f2mul(pw, a2);
     }
     if (xok) {
       const float Q = Q2.x + Q2.y, P = P2.x + P2.y;

@@ -194,18 +194,59 @@ void retain_pool() {
   done[dev] = true;
 }
 
-// Per-device copy-in / copy-out streams of gc_filter_host (created once, never destroyed).
-bool copy_streams(cudaStream_t* sin, cudaStream_t* sout) {
+// Per-device copy-in / copy-out streams and a second compute stream of gc_filter_host
+// (created once, never destroyed).
+bool host_streams(cudaStream_t* sin, cudaStream_t* sout, cudaStream_t* sc) {
   static std::mutex mu;
-  static cudaStream_t tab[64][2] = {};
+  static cudaStream_t tab[64][3] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
   std::lock_guard<std::mutex> lk(mu);
-  for (int i = 0; i < 2; i++)
+  for (int i = 0; i < 3; i++)
     if (!tab[dev][i] && cudaStreamCreateWithFlags(&tab[dev][i], cudaStreamNonBlocking) != cudaSuccess) return false;
   *sin = tab[dev][0];
   *sout = tab[dev][1];
+  *sc = tab[dev][2];
   return true;
+}
+
+// Per-device free list of timing-disabled events for gc_filter_host (creating and destroying
+// 2K+2 events per call costs more than a small image's kernels).  Events taken by a call are
+// private to it until returned.
+struct EventPool {
+  std::mutex mu;
+  std::vector<cudaEvent_t> free_[64];
+  bool take(int n, std::vector<cudaEvent_t>& out) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+    std::lock_guard<std::mutex> lk(mu);
+    auto& f = free_[dev];
+    out.clear();
+    while ((int)out.size() < n && !f.empty()) {
+      out.push_back(f.back());
+      f.pop_back();
+    }
+    while ((int)out.size() < n) {
+      cudaEvent_t ev = nullptr;
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+        for (auto e : out) f.push_back(e);
+        out.clear();
+        return false;
+      }
+      out.push_back(ev);
+    }
+    return true;
+  }
+  void give(const std::vector<cudaEvent_t>& evs) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto e : evs) free_[dev].push_back(e);
+  }
+};
+EventPool& event_pool() {
+  static EventPool p;
+  return p;
 }
 
 // Run the pipeline for the window described by k (rows/segments already set).
@@ -483,51 +524,56 @@ gc_status gc_filter_host(const float* imgs_host, int B, int H, int W, const gc_p
   // neighbouring chunks' copies).  Results are identical to gc_filter up to the O(1)
   // operator's segment-dependent rounding (FIR: bit-identical).
   const int R = halo_of(p);
-  // chunks of >= ~2 MB (smaller copies do not amortise their launch and event costs)
-  int K = (int)std::max<size_t>(1, std::min<size_t>(8, bytes / (2u << 20)));
-  if (B > 1) K = std::min(K, B);
-  else K = std::max(1, std::min(K, H / std::max(1, 8 * R)));
+  // chunks of >= 1 MB, at most 8 for batches, and for row bands >= max(8 R, 64) rows
+  // (measured on B200, tools/host_timing1.py, profiles/r01_e2e_host_chunks.txt: c2 4 chunks
+  // 211 us vs 2: 222, 8: 281; c5 16 chunks 25.7 ms vs 8: 29.5, 32: 26.8; c1 1 chunk 76 us
+  // vs 2: 104; c4 x32 8 chunks 3.79 ms vs 16: 3.92)
+  int K = (int)std::max<size_t>(1, std::min<size_t>(16, bytes / (1u << 20)));
+  if (B > 1) K = std::min(std::min(K, 8), B);
+  else K = std::max(1, std::min(K, H / std::max(64, 8 * R)));
   if (const char* env = std::getenv("GC_HOST_CHUNKS")) K = std::max(1, std::min(atoi(env), B > 1 ? B : H));
-  cudaStream_t sin = nullptr, sout = nullptr;
-  std::vector<cudaEvent_t> ev_in(K, nullptr), ev_comp(K, nullptr);
-  cudaEvent_t ev_start = nullptr, ev_done = nullptr;
-  bool ok = copy_streams(&sin, &sout) &&
-            cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming) == cudaSuccess &&
-            cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) == cudaSuccess;
-  for (int k = 0; ok && k < K; k++)
-    ok = cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming) == cudaSuccess &&
-         cudaEventCreateWithFlags(&ev_comp[k], cudaEventDisableTiming) == cudaSuccess;
+  cudaStream_t sin = nullptr, sout = nullptr, sc = nullptr;
+  std::vector<cudaEvent_t> evs;
+  const bool ok = host_streams(&sin, &sout, &sc) && event_pool().take(2 * K + 3, evs);
+  cudaEvent_t* ev_in = ok ? evs.data() : nullptr;
+  cudaEvent_t* ev_comp = ok ? evs.data() + K : nullptr;
+  cudaEvent_t ev_start = ok ? evs[2 * K] : nullptr, ev_done = ok ? evs[2 * K + 1] : nullptr;
+  cudaEvent_t ev_c2 = ok ? evs[2 * K + 2] : nullptr;
   if (!ok) {
     st = GC_ECUDA;
   } else {
-    // chunk k = [c0[k], c0[k+1]) images (B > 1) or rows (B = 1)
+    // output chunk k = [c0[k], c0[k+1]) images (B > 1) or rows (B = 1).  For row bands the
+    // input chunks are shifted down by the halo, h[k] = c0[k] + R, so that band k reads only
+    // input chunks 0..k and starts as soon as chunk k has arrived.
     const int n = B > 1 ? B : H;
-    std::vector<int> c0(K + 1);
+    std::vector<int> c0(K + 1), h(K + 1);
     for (int k = 0; k <= K; k++) c0[k] = (int)((long long)n * k / K);
+    for (int k = 0; k <= K; k++) h[k] = (B > 1 || k == 0 || k == K) ? c0[k] : std::min(n, c0[k] + R);
     const size_t unit = B > 1 ? (size_t)H * W : (size_t)W;     // floats per image / per row
     cudaEventRecord(ev_start, s);                                // device buffers allocated
     cudaStreamWaitEvent(sin, ev_start, 0);
+    cudaStreamWaitEvent(sc, ev_start, 0);
     for (int k = 0; k < K && e == cudaSuccess; k++) {
-      const size_t off = (size_t)c0[k] * unit, cnt = (size_t)(c0[k + 1] - c0[k]) * unit;
-      e = cudaMemcpyAsync(din + off, imgs_host + off, cnt * 4, cudaMemcpyHostToDevice, sin);
+      const size_t off = (size_t)h[k] * unit, cnt = (size_t)(h[k + 1] - h[k]) * unit;
+      if (cnt) e = cudaMemcpyAsync(din + off, imgs_host + off, cnt * 4, cudaMemcpyHostToDevice, sin);
       if (e == cudaSuccess) e = cudaEventRecord(ev_in[k], sin);
     }
+    // row bands alternate between two compute streams, so a band's kernels overlap the
+    // previous band's tail (a band of one image does not fill the GPU on its own; image
+    // chunks of a batch do, and stay on `s`)
     for (int k = 0; k < K && e == cudaSuccess && st == GC_OK; k++) {
+      cudaStream_t sk = (B == 1 && (k & 1)) ? sc : s;
+      cudaStreamWaitEvent(sk, ev_in[k], 0);                     // input chunks 0..k have arrived
       if (B > 1) {
-        cudaStreamWaitEvent(s, ev_in[k], 0);
-        st = gc_filter(din + (size_t)c0[k] * unit, c0[k + 1] - c0[k], H, W, p, dout + (size_t)c0[k] * unit, stream);
+        st = gc_filter(din + (size_t)c0[k] * unit, c0[k + 1] - c0[k], H, W, p, dout + (size_t)c0[k] * unit, sk);
       } else {
-        const int need = std::min(H - 1, c0[k + 1] - 1 + R);    // last input row the band reads
-        int j = k;
-        while (j + 1 < K && c0[j + 1] <= need) j++;
-        cudaStreamWaitEvent(s, ev_in[j], 0);                    // chunks 0..j have arrived
         const float* seg[3] = {din, din, din};
         const int seg_row0[3] = {0, -1, -1};
         const int seg_rows[3] = {H, 0, 0};
         st = gc_filter_window(seg, seg_row0, seg_rows, H, W, c0[k], c0[k + 1] - c0[k], p,
-                              dout + (size_t)c0[k] * unit, stream);
+                              dout + (size_t)c0[k] * unit, sk);
       }
-      if (st == GC_OK) e = cudaEventRecord(ev_comp[k], s);
+      if (st == GC_OK) e = cudaEventRecord(ev_comp[k], sk);
     }
     for (int k = 0; k < K && e == cudaSuccess && st == GC_OK; k++) {
       const size_t off = (size_t)c0[k] * unit, cnt = (size_t)(c0[k + 1] - c0[k]) * unit;
@@ -536,18 +582,15 @@ gc_status gc_filter_host(const float* imgs_host, int B, int H, int W, const gc_p
     }
     cudaEventRecord(ev_done, sout);
     cudaEventRecord(ev_start, sin);
+    cudaEventRecord(ev_c2, sc);
     cudaStreamWaitEvent(s, ev_done, 0);                          // buffers free only after all
-    cudaStreamWaitEvent(s, ev_start, 0);                         // copies on both streams
+    cudaStreamWaitEvent(s, ev_start, 0);                         // copies and both compute
+    cudaStreamWaitEvent(s, ev_c2, 0);                            // streams
   }
   cudaFreeAsync(din, s);
   cudaFreeAsync(dout, s);
   cudaError_t es = cudaStreamSynchronize(s);
-  for (int k = 0; k < K; k++) {
-    if (ev_in[k]) cudaEventDestroy(ev_in[k]);
-    if (ev_comp[k]) cudaEventDestroy(ev_comp[k]);
-  }
-  if (ev_start) cudaEventDestroy(ev_start);
-  if (ev_done) cudaEventDestroy(ev_done);
+  if (ok) event_pool().give(evs);
   if (st != GC_OK) return st;
   if (e != cudaSuccess) return cuda_status(e);
   return cuda_status(es);

@@ -135,3 +135,29 @@ def test_deriche_is_not_eq7(gc):
     dr = gc.filter(t, 5.0, c.sigma_r_twin, c.N, op=OP_DERICHE).cpu().numpy().astype(np.float64)
     ref, _ = oracle.gc_filter(img, 5.0, c.sigma_r_twin, c.N)
     assert np.max(np.abs(dr - ref)) > 0.05
+
+
+def test_band_path_single_rank_nccl_deriche(gc):
+    """gc_bilateral_band with the Deriche operator (halos of K = ceil(10 s) rows) through a
+    real one-rank NCCL communicator: the band is the whole image, bit for bit gc_filter."""
+    import os
+    import torch
+    import torch.distributed as dist
+    own = not dist.is_initialized()
+    if own:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    c = CONFIGS["c5"]
+    img = config_image(c, H=180, W=150)
+    t = torch.from_numpy(img).cuda()
+    whole = gc.filter(t, 3.0, c.sigma_r_twin, c.N, op=OP_DERICHE)
+    comm = gc.Comm(0, 1)
+    try:
+        band = gc.bilateral_band(t, 180, 0, 3.0, c.sigma_r_twin, c.N, comm, op=OP_DERICHE)
+        torch.cuda.synchronize()
+        assert torch.equal(band, whole)
+    finally:
+        comm.close()
+        if own:
+            dist.destroy_process_group()

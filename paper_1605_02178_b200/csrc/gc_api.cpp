@@ -5,6 +5,8 @@
 // arguments.  There is no CPU fallback: if the device path cannot run, the call fails
 // with a status code.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -511,6 +513,9 @@ gc_status gc_filter_host(const float* imgs_host, int B, int H, int W, const gc_p
   if (st != GC_OK) return st;
   if (!imgs_host || !outs_host || B < 1 || H < 1 || W < 1) return GC_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // GC_HOST_TRACE=1: print the pipeline's device timeline and host enqueue time (development)
+  static const bool trace = std::getenv("GC_HOST_TRACE") != nullptr;
+  const auto t_host0 = std::chrono::steady_clock::now();
   const size_t bytes = (size_t)B * H * W * sizeof(float);
   float *din = nullptr, *dout = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&din, bytes, s);
@@ -524,16 +529,17 @@ gc_status gc_filter_host(const float* imgs_host, int B, int H, int W, const gc_p
   // neighbouring chunks' copies).  Results are identical to gc_filter up to the O(1)
   // operator's segment-dependent rounding (FIR: bit-identical).
   const int R = halo_of(p);
-  // chunks of >= 1 MB, at most 8 for batches, and for row bands >= max(8 R, 64) rows
-  // (measured on B200, tools/host_timing1.py, profiles/r01_e2e_host_chunks.txt: c2 4 chunks
-  // 211 us vs 2: 222, 8: 281; c5 16 chunks 25.7 ms vs 8: 29.5, 32: 26.8; c1 1 chunk 76 us
-  // vs 2: 104; c4 x32 8 chunks 3.79 ms vs 16: 3.92)
-  int K = (int)std::max<size_t>(1, std::min<size_t>(16, bytes / (1u << 20)));
+  // chunks of >= 2 MB, at most 8 for batches, and for row bands >= max(8 R, 64) rows
+  // (measured on B200, tools/host_timing1.py, profiles/r01_e2e_host_chunks.txt: c2 device
+  // timeline 171 us with 2 chunks vs 193 with 4 and 207 with 1 (GC_HOST_TRACE; H2D and D2H
+  // barely overlap on this PCIe link, so 8 MB of copies take >= 155 us); c5 16 chunks 25.7 ms
+  // vs 8: 29.5, 32: 26.8; c1 1 chunk 76 us vs 2: 104; c4 x32 8 chunks 3.79 ms vs 16: 3.92)
+  int K = (int)std::max<size_t>(1, std::min<size_t>(16, bytes / (2u << 20)));
   if (B > 1) K = std::min(std::min(K, 8), B);
   else K = std::max(1, std::min(K, H / std::max(64, 8 * R)));
   if (const char* env = std::getenv("GC_HOST_CHUNKS")) K = std::max(1, std::min(atoi(env), B > 1 ? B : H));
   cudaStream_t sin = nullptr, sout = nullptr, sc = nullptr;
-  std::vector<cudaEvent_t> evs;
+  std::vector<cudaEvent_t> evs, tr;
   const bool ok = host_streams(&sin, &sout, &sc) && event_pool().take(2 * K + 3, evs);
   cudaEvent_t* ev_in = ok ? evs.data() : nullptr;
   cudaEvent_t* ev_comp = ok ? evs.data() + K : nullptr;
@@ -553,10 +559,16 @@ gc_status gc_filter_host(const float* imgs_host, int B, int H, int W, const gc_p
     cudaEventRecord(ev_start, s);                                // device buffers allocated
     cudaStreamWaitEvent(sin, ev_start, 0);
     cudaStreamWaitEvent(sc, ev_start, 0);
+    if (trace) {
+      tr.resize(3 * K + 1);
+      for (auto& ev : tr) cudaEventCreate(&ev);
+      cudaEventRecord(tr[0], s);
+    }
     for (int k = 0; k < K && e == cudaSuccess; k++) {
       const size_t off = (size_t)h[k] * unit, cnt = (size_t)(h[k + 1] - h[k]) * unit;
       if (cnt) e = cudaMemcpyAsync(din + off, imgs_host + off, cnt * 4, cudaMemcpyHostToDevice, sin);
       if (e == cudaSuccess) e = cudaEventRecord(ev_in[k], sin);
+      if (trace) cudaEventRecord(tr[1 + k], sin);
     }
     // row bands alternate between two compute streams, so a band's kernels overlap the
     // previous band's tail (a band of one image does not fill the GPU on its own; image
@@ -574,11 +586,13 @@ gc_status gc_filter_host(const float* imgs_host, int B, int H, int W, const gc_p
                               dout + (size_t)c0[k] * unit, sk);
       }
       if (st == GC_OK) e = cudaEventRecord(ev_comp[k], sk);
+      if (trace) cudaEventRecord(tr[1 + K + k], sk);
     }
     for (int k = 0; k < K && e == cudaSuccess && st == GC_OK; k++) {
       const size_t off = (size_t)c0[k] * unit, cnt = (size_t)(c0[k + 1] - c0[k]) * unit;
       cudaStreamWaitEvent(sout, ev_comp[k], 0);
       e = cudaMemcpyAsync(outs_host + off, dout + off, cnt * 4, cudaMemcpyDeviceToHost, sout);
+      if (trace) cudaEventRecord(tr[1 + 2 * K + k], sout);
     }
     cudaEventRecord(ev_done, sout);
     cudaEventRecord(ev_start, sin);
@@ -589,8 +603,26 @@ gc_status gc_filter_host(const float* imgs_host, int B, int H, int W, const gc_p
   }
   cudaFreeAsync(din, s);
   cudaFreeAsync(dout, s);
+  const auto t_host1 = std::chrono::steady_clock::now();
   cudaError_t es = cudaStreamSynchronize(s);
   if (ok) event_pool().give(evs);
+  if (trace && !tr.empty()) {
+    const auto t_host2 = std::chrono::steady_clock::now();
+    auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    std::fprintf(stderr, "gc_filter_host K=%d: host enqueue %.1f us, sync wait %.1f us | device (us from start):", K,
+                 us(t_host0, t_host1), us(t_host1, t_host2));
+    const char* what[3] = {"h2d", "comp", "d2h"};
+    for (int w = 0; w < 3; w++) {
+      std::fprintf(stderr, " %s", what[w]);
+      for (int k = 0; k < K; k++) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, tr[0], tr[1 + w * K + k]);
+        std::fprintf(stderr, " %.1f", 1e3f * ms);
+      }
+    }
+    std::fprintf(stderr, "\n");
+    for (auto ev : tr) cudaEventDestroy(ev);
+  }
   if (st != GC_OK) return st;
   if (e != cudaSuccess) return cuda_status(e);
   return cuda_status(es);

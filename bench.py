@@ -349,9 +349,10 @@ def main():
         hin = torch.from_numpy(x.cpu().numpy()).pin_memory()
         hout = torch.empty_like(hin).pin_memory()
         hin_np, hout_np = hin.numpy(), hout.numpy()
-        # the host<->device path needs ~100 calls (~20 ms) to reach its steady rate (stream-ordered
-        # pool, PCIe and host power states; tools/e2e_probe.py): warm it for 30 ms of calls
-        t_end = time.perf_counter() + 0.03
+        # DMA to freshly pinned host buffers is slow until the host side has warmed them (per-buffer
+        # ramps of hundreds of calls on the B200 VMs, profiles/r01_e2e_host_chunks.txt): warm the
+        # e2e leg with 0.5 s of calls on the buffers it times
+        t_end = time.perf_counter() + 0.5
         for _ in range(max(3, args.warmup)):
             gc.filter_host(hin_np, sigma_s, sigma_r, cfg.N, out=hout_np, op=args.op)
         while time.perf_counter() < t_end:

@@ -57,25 +57,6 @@ void o1_constants(float sigma_s, KParams& k) {
   }
 }
 
-// Segment lengths of the O(1) passes: enough warps to fill the GPU (~16 per SM), segments no
-// shorter than 4 lead-ins (2W+1 samples each) unless the image itself is shorter.
-void o1_segments(KParams& k) {
-  const int target = k.num_sms * 16;
-  const int lead = 2 * k.R + 1;
-  auto split = [&](int len, long long base, int& seg, int& nseg) {
-    long long want = (target + base - 1) / base;
-    long long cap = std::max(1, len / (4 * lead));
-    int n = (int)std::max(1LL, std::min(want, cap));
-    seg = ((len + n - 1) / n + 31) / 32 * 32;
-    nseg = (len + seg - 1) / seg;
-  };
-  k.o1_groups = (k.NP + 3) / 4;
-  split(k.Wd, (long long)((k.in_rows + 31) / 32) * k.o1_groups * k.B, k.o1_seg_x, k.o1_nseg_x);
-  int G, npg;
-  o1_col_split(k.NP, G, npg);
-  split(k.out_rows, (long long)((k.Wd + 32 / G - 1) / (32 / G)) * k.B, k.o1_seg_y, k.o1_nseg_y);
-}
-
 gc_status validate_params(const gc_params* p) {
   if (!p) return GC_EINVAL;
   if (p->N < 0) return GC_EINVAL;
@@ -259,7 +240,6 @@ gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) 
   k.num_sms = 148;
   cudaDeviceGetAttribute(&k.num_sms, cudaDevAttrMultiProcessorCount, dev);
   const int op = k.op;
-  if (op == GC_OP_O1) o1_segments(k);
   if (op == GC_OP_DERICHE) dr_segments(k);
   const size_t plane_elems = (size_t)k.NP * k.in_rows * k.Wd;
   float2* planes = nullptr;

@@ -490,22 +490,61 @@ bool make_o1_plane_map(CUtensorMap* map, const KParams& p) {
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Segments of a line of `len` samples for `base` independent lines (tasks = base x segments),
+// each segment paying a lead-in of `lead` samples, on a GPU holding `resident` warps at once:
+// the count minimising waves x (segment + lead-in), i.e. the last wave's tail against the
+// lead-in overhead (measured on B200: c5 column pass 8.89 ms with the former fixed target of
+// 16 warps/SM vs 7.65 ms at the chosen 16 segments; c3 sigma_s = 40 0.876 -> 0.623 ms;
+// profiles/r01_ab_experiments.md).  Segments are multiples of 32 samples.
+void o1_pick_segments(int len, long long base, int lead, long long resident, int& seg, int& nseg) {
+  resident = std::max(1LL, resident);
+  const int nmax = std::max(1, std::min(256, len / std::max(1, lead)));
+  double best = 0;
+  seg = (len + 31) / 32 * 32;
+  nseg = 1;
+  for (int n = 1; n <= nmax; n++) {
+    const int sg = ((len + n - 1) / n + 31) / 32 * 32;
+    const int nn = (len + sg - 1) / sg;
+    const long long waves = (base * nn + resident - 1) / resident;
+    const double t = (double)waves * (double)(sg + lead);
+    if (n == 1 || t < best * 0.999) {
+      best = t;
+      seg = sg;
+      nseg = nn;
+    }
+  }
+}
+
+// Resident warps of `kern` on the whole GPU (blocks of kO1Warps warps, `smem` bytes each).
+template <typename K>
+long long o1_resident_warps(K kern, size_t smem, int num_sms) {
+  int blocks = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, 32 * kO1Warps, smem) != cudaSuccess) blocks = 1;
+  return (long long)std::max(1, blocks) * kO1Warps * num_sms;
+}
+
 template <int NPG, int G>
-cudaError_t launch_col(const KParams& p, cudaStream_t s) {
+cudaError_t launch_col(const KParams& p0, cudaStream_t s) {
   constexpr int CW = 32 / G;
-  const long long nt = (long long)((p.Wd + CW - 1) / CW) * p.o1_nseg_y * p.B;
-  const unsigned grid = (unsigned)((nt + kO1Warps - 1) / kO1Warps);
   CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
-  const bool tma = G == 1 && p.NP <= NPG && (p.Wd & 1) == 0 && make_o1_plane_map(&map, p);
+  const bool tma = G == 1 && p0.NP <= NPG && (p0.Wd & 1) == 0 && make_o1_plane_map(&map, p0);
   auto kern = tma ? k_col_o1<NPG, G, true> : k_col_o1<NPG, G, false>;
+  const size_t smem = kO1Warps * sizeof(ColO1Smem);
   static std::atomic<unsigned long long> ready[2];  // > 48 KB dynamic shared memory: opt in per device
+  static std::atomic<long long> resident[2];        // (same device class for every device in a box)
   const cudaError_t e = once_per_device(ready[tma], [&]() {
-    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kO1Warps * sizeof(ColO1Smem)));
+    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (r == cudaSuccess) resident[tma].store(o1_resident_warps(kern, smem, p0.num_sms));
+    return r;
   });
   if (e != cudaSuccess) return e;
-  return launch_k(kern, dim3(grid), dim3(32 * kO1Warps), kO1Warps * sizeof(ColO1Smem), s, p.ev[1] == nullptr,
-                  map, p);
+  KParams p = p0;
+  const long long ncb = (p.Wd + CW - 1) / CW;
+  o1_pick_segments(p.out_rows, ncb * p.B, 2 * p.R + 1, resident[tma].load(), p.o1_seg_y, p.o1_nseg_y);
+  const long long nt = ncb * p.o1_nseg_y * p.B;
+  const unsigned grid = (unsigned)((nt + kO1Warps - 1) / kO1Warps);
+  return launch_k(kern, dim3(grid), dim3(32 * kO1Warps), smem, s, p.ev[1] == nullptr, map, p);
 }
 
 template <int G, int LO, int HI>
@@ -520,17 +559,24 @@ cudaError_t launch_col_g(const KParams& p, int npg, cudaStream_t s) {
 
 }  // namespace
 
-cudaError_t launch_o1_two_pass(const KParams& p, cudaStream_t s) {
-  // row pass
+cudaError_t launch_o1_two_pass(const KParams& p0, cudaStream_t s) {
+  // row pass: warp tasks = 32 rows x one x-segment x one group of <= 4 plane pairs
   const size_t smem_r = (size_t)kO1Warps * sizeof(RowO1Smem);
   static std::atomic<unsigned long long> ready{0};
+  static std::atomic<long long> resident_r{1};
   {
     const cudaError_t e = once_per_device(ready, [&]() {
-      return cudaFuncSetAttribute(k_row_o1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r);
+      cudaError_t r = cudaFuncSetAttribute(k_row_o1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r);
+      if (r == cudaSuccess) resident_r.store(o1_resident_warps(k_row_o1, smem_r, p0.num_sms));
+      return r;
     });
     if (e != cudaSuccess) return e;
   }
-  const long long ntr = (long long)((p.in_rows + 31) / 32) * p.o1_nseg_x * p.o1_groups * p.B;
+  KParams p = p0;
+  p.o1_groups = (p.NP + kO1RowNPG - 1) / kO1RowNPG;
+  const long long nrb = (p.in_rows + 31) / 32;
+  o1_pick_segments(p.Wd, nrb * p.o1_groups * p.B, 2 * p.R + 1, resident_r.load(), p.o1_seg_x, p.o1_nseg_x);
+  const long long ntr = nrb * p.o1_nseg_x * p.o1_groups * p.B;
   if (p.ev[0]) cudaEventRecord(p.ev[0], s);
   k_row_o1<<<(unsigned)((ntr + kO1Warps - 1) / kO1Warps), 32 * kO1Warps, smem_r, s>>>(p);
   cudaError_t e = cudaGetLastError();

@@ -144,22 +144,6 @@ gc_status cuda_status(cudaError_t e) {
   return GC_ECUDA;
 }
 
-// Segment lengths of the Deriche passes (gc_deriche.cu): ~16 warps per SM where the image
-// allows, segments no shorter than two lead-ins (K = ceil(10 sigma_s) samples each);
-// row-pass segments are multiples of 8 columns (shared-memory store chunks).
-void dr_segments(KParams& k) {
-  const int target = k.num_sms * 16;
-  auto split = [&](int len, long long base, int align, int& seg, int& nseg) {
-    long long want = (target + base - 1) / base;
-    long long cap = std::max(1, len / (2 * k.dr_K));
-    int n = (int)std::max(1LL, std::min(want, cap));
-    seg = ((len + n - 1) / n + align - 1) / align * align;
-    nseg = (len + seg - 1) / seg;
-  };
-  split(k.Wd, (long long)((k.in_rows + 31) / 32) * k.B, 8, k.dr_seg_x, k.dr_nseg_x);
-  split(k.out_rows, (long long)((k.Wd + 31) / 32) * k.B, 1, k.dr_seg_y, k.dr_nseg_y);
-}
-
 // Keep freed stream-ordered scratch in the device's default pool instead of returning it
 // to the driver at every synchronisation (the plane buffer is reallocated per call).
 void retain_pool() {
@@ -240,7 +224,6 @@ gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) 
   k.num_sms = 148;
   cudaDeviceGetAttribute(&k.num_sms, cudaDevAttrMultiProcessorCount, dev);
   const int op = k.op;
-  if (op == GC_OP_DERICHE) dr_segments(k);
   const size_t plane_elems = (size_t)k.NP * k.in_rows * k.Wd;
   float2* planes = nullptr;
   float2* taps_dev = nullptr;

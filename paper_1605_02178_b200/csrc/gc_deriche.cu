@@ -404,14 +404,32 @@ __global__ void __launch_bounds__(32 * kDrWarps) k_col_dr(const KParams p) {
 
 namespace {
 
+template <typename K>
+long long dr_resident_warps(K kern, size_t smem, int num_sms) {
+  int blocks = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, 32 * kDrWarps, smem) != cudaSuccess) blocks = 1;
+  return (long long)std::max(1, blocks) * kDrWarps * num_sms;
+}
+
 template <int NPG>
-cudaError_t launch_dr(const KParams& p, cudaStream_t s) {
+cudaError_t launch_dr(const KParams& p0, cudaStream_t s) {
   const size_t smem_r = (size_t)kDrWarps * sizeof(DrRowSmem);
   static std::atomic<unsigned long long> ready{0};
+  static std::atomic<long long> res_r{1}, res_c{1};
   cudaError_t e = once_per_device(ready, [&]() {
-    return cudaFuncSetAttribute(k_row_dr<NPG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r);
+    cudaError_t r = cudaFuncSetAttribute(k_row_dr<NPG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r);
+    if (r == cudaSuccess) {
+      res_r.store(dr_resident_warps(k_row_dr<NPG>, smem_r, p0.num_sms));
+      res_c.store(dr_resident_warps(k_col_dr<NPG>, 0, p0.num_sms));
+    }
+    return r;
   });
   if (e != cudaSuccess) return e;
+  // segments: lead-in K per sweep direction; row-pass segments are multiples of the 8-column chunk
+  KParams p = p0;
+  pick_segments(p.Wd, (long long)((p.in_rows + 31) / 32) * p.B, p.dr_K, res_r.load(), kDrChunk, p.dr_seg_x,
+                p.dr_nseg_x);
+  pick_segments(p.out_rows, (long long)((p.Wd + 31) / 32) * p.B, p.dr_K, res_c.load(), 1, p.dr_seg_y, p.dr_nseg_y);
   const long long ntr = (long long)((p.in_rows + 31) / 32) * p.dr_nseg_x * p.B;
   const long long ntc = (long long)((p.Wd + 31) / 32) * p.dr_nseg_y * p.B;
   if (p.ev[0]) cudaEventRecord(p.ev[0], s);

@@ -103,6 +103,31 @@ inline void o1_col_split(int NP, int& G, int& npg) {
   npg = (NP + G - 1) / G;
 }
 
+// Segments of a line of `len` samples for `base` independent lines (tasks = base x segments),
+// each segment paying a lead-in of `lead` samples, on a GPU that holds `resident` warps at once:
+// the count minimising waves x (segment + lead-in), i.e. the last wave's tail against the
+// lead-in overhead (O(1) and Deriche passes; measured on B200 in profiles/r01_ab_experiments.md).
+// Segments are multiples of `align` samples.
+inline void pick_segments(int len, long long base, int lead, long long resident, int align, int& seg, int& nseg) {
+  resident = resident < 1 ? 1 : resident;
+  int nmax = len / (lead < 1 ? 1 : lead);
+  nmax = nmax < 1 ? 1 : (nmax > 256 ? 256 : nmax);
+  double best = 0;
+  seg = (len + align - 1) / align * align;
+  nseg = 1;
+  for (int n = 1; n <= nmax; n++) {
+    const int sg = ((len + n - 1) / n + align - 1) / align * align;
+    const int nn = (len + sg - 1) / sg;
+    const long long waves = (base * nn + resident - 1) / resident;
+    const double t = (double)waves * (double)(sg + lead);
+    if (n == 1 || t < best * 0.999) {
+      best = t;
+      seg = sg;
+      nseg = nn;
+    }
+  }
+}
+
 // Per-device one-time setup (function attributes are per device context): run fn once per
 // (call site, device); fn must be idempotent (two threads may both run it once).
 template <typename F>

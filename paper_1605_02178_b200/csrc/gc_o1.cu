@@ -490,31 +490,6 @@ bool make_o1_plane_map(CUtensorMap* map, const KParams& p) {
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Segments of a line of `len` samples for `base` independent lines (tasks = base x segments),
-// each segment paying a lead-in of `lead` samples, on a GPU holding `resident` warps at once:
-// the count minimising waves x (segment + lead-in), i.e. the last wave's tail against the
-// lead-in overhead (measured on B200: c5 column pass 8.89 ms with the former fixed target of
-// 16 warps/SM vs 7.65 ms at the chosen 16 segments; c3 sigma_s = 40 0.876 -> 0.623 ms;
-// profiles/r01_ab_experiments.md).  Segments are multiples of 32 samples.
-void o1_pick_segments(int len, long long base, int lead, long long resident, int& seg, int& nseg) {
-  resident = std::max(1LL, resident);
-  const int nmax = std::max(1, std::min(256, len / std::max(1, lead)));
-  double best = 0;
-  seg = (len + 31) / 32 * 32;
-  nseg = 1;
-  for (int n = 1; n <= nmax; n++) {
-    const int sg = ((len + n - 1) / n + 31) / 32 * 32;
-    const int nn = (len + sg - 1) / sg;
-    const long long waves = (base * nn + resident - 1) / resident;
-    const double t = (double)waves * (double)(sg + lead);
-    if (n == 1 || t < best * 0.999) {
-      best = t;
-      seg = sg;
-      nseg = nn;
-    }
-  }
-}
-
 // Resident warps of `kern` on the whole GPU (blocks of kO1Warps warps, `smem` bytes each).
 template <typename K>
 long long o1_resident_warps(K kern, size_t smem, int num_sms) {
@@ -541,7 +516,7 @@ cudaError_t launch_col(const KParams& p0, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   KParams p = p0;
   const long long ncb = (p.Wd + CW - 1) / CW;
-  o1_pick_segments(p.out_rows, ncb * p.B, 2 * p.R + 1, resident[tma].load(), p.o1_seg_y, p.o1_nseg_y);
+  pick_segments(p.out_rows, ncb * p.B, 2 * p.R + 1, resident[tma].load(), 32, p.o1_seg_y, p.o1_nseg_y);
   const long long nt = ncb * p.o1_nseg_y * p.B;
   const unsigned grid = (unsigned)((nt + kO1Warps - 1) / kO1Warps);
   return launch_k(kern, dim3(grid), dim3(32 * kO1Warps), smem, s, p.ev[1] == nullptr, map, p);
@@ -575,7 +550,7 @@ cudaError_t launch_o1_two_pass(const KParams& p0, cudaStream_t s) {
   KParams p = p0;
   p.o1_groups = (p.NP + kO1RowNPG - 1) / kO1RowNPG;
   const long long nrb = (p.in_rows + 31) / 32;
-  o1_pick_segments(p.Wd, nrb * p.o1_groups * p.B, 2 * p.R + 1, resident_r.load(), p.o1_seg_x, p.o1_nseg_x);
+  pick_segments(p.Wd, nrb * p.o1_groups * p.B, 2 * p.R + 1, resident_r.load(), 32, p.o1_seg_x, p.o1_nseg_x);
   const long long ntr = nrb * p.o1_nseg_x * p.o1_groups * p.B;
   if (p.ev[0]) cudaEventRecord(p.ev[0], s);
   k_row_o1<<<(unsigned)((ntr + kO1Warps - 1) / kO1Warps), 32 * kO1Warps, smem_r, s>>>(p);

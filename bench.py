@@ -86,8 +86,8 @@ DR_FLOP_PER_PLANE = 35  # Deriche mode per plane-sample and pass: 2 sections x 4
 
 
 def resolve_op(op, R):
-    """GC_OP_AUTO -> FIR for W_s <= 16, O(1) above (include/gc.h, gc_api.cpp)."""
-    return op if op in (1, 2, 3) else (2 if R >= 17 else 1)
+    """GC_OP_AUTO -> FIR for W_s <= 24, O(1) above (include/gc.h, gc_api.cpp)."""
+    return op if op in (1, 2, 3) else (2 if R >= 25 else 1)
 
 
 def op_flop_per_plane(op, R):

@@ -59,7 +59,7 @@ typedef enum {
    exactly as eq. (7) writes it (R3); they differ only in cost and rounding.
    DERICHE replaces it by the recursive filter the paper cites for its O(1) claim. */
 typedef enum {
-  GC_OP_AUTO = 0,  /* library choice by W_s: FIR for W_s <= 16, O1 above  */
+  GC_OP_AUTO = 0,  /* library choice by W_s: FIR for W_s <= 24, O1 above  */
   GC_OP_FIR = 1,   /* direct separable FIR, 2(2W_s+1) FMA per plane-pixel; W_s <= 1024   */
   GC_OP_O1 = 2,    /* exact-window O(1) recursion: the truncated window of eq. (7) with
                       the taps replaced by a 6-term cosine least-squares fit (max error

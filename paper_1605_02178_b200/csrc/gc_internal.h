@@ -22,7 +22,7 @@ constexpr int kMaxTemplW = 24;                 // FIR radius range with unrolled
 constexpr int kMaxFirW = 1024;                 // runtime-W FIR kernels (taps in global)
 constexpr int kO1K = 6;                        // O(1) operator: cosine terms (q = 0 is the box)
 constexpr int kO1MaxW = 4096;                  // O(1) operator radius limit
-constexpr int kO1AutoMinW = 17;                // GC_OP_AUTO: FIR for W <= 16, O(1) above
+constexpr int kO1AutoMinW = kMaxTemplW + 1;     // GC_OP_AUTO: FIR for W <= 24 (unrolled kernels), O(1) above
 
 // One input-row segment (device pointer to rows [row0, row0+rows) of the global image).
 struct Seg {

@@ -156,4 +156,4 @@ def test_operator_taps(gc, sigma_s):
     assert abs(o1.sum() - 1.0) <= 1e-5
     assert np.allclose(o1, o1[::-1], rtol=0, atol=1e-15)            # symmetric (cosines)
     auto = gc.operator_taps(sigma_s, gc.OP_AUTO)
-    assert np.array_equal(auto, o1 if W >= 17 else fir)
+    assert np.array_equal(auto, o1 if W >= 25 else fir)

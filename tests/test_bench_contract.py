@@ -37,7 +37,7 @@ def test_flop_accounting():
     assert bench.flops_col(N, R, px, 1) == px * (10 * 62 + 6 * 9 + 8)
     assert bench.flops_col(N, R, px, 2) == px * (10 * 50 + 6 * 9 + 8)
     assert bench.op_flop_per_plane(3, R) == 35
-    assert bench.resolve_op(0, 16) == 1 and bench.resolve_op(0, 17) == 2 and bench.resolve_op(3, 5) == 3
+    assert bench.resolve_op(0, 24) == 1 and bench.resolve_op(0, 25) == 2 and bench.resolve_op(3, 5) == 3
 
 
 @pytest.mark.parametrize("N,NP", [(5, 4), (8, 5), (12, 7)])

@@ -404,7 +404,7 @@ def main():
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             try:
-                key = f"{cfg.name}_s{sigma_s:g}_{'o1' if op == 2 else 'fir'}:{dom}"
+                key = f"{cfg.name}_s{sigma_s:g}_{ {1: 'fir', 2: 'o1', 3: 'deriche'}[op]}:{dom}"
                 traffic = json.load(open(tp)).get(key)
             except Exception:
                 traffic = None

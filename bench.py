@@ -412,10 +412,14 @@ def main():
                 "frac": ach / FP32_PEAK_TFLOPS, "traffic": traffic,
                 "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP x 1.965 GHz (B200_PROFILING.md unit "
                                "counts; FFMA measured at 125-128 lanes/clk/SM, profiles/r01_ubench_fp32.txt)"}
+        if traffic:
+            roof["traffic_bytes_per_px"] = traffic / (B * H * W)     # DRAM bytes per output pixel (ncu)
         if op == 3 and kernels[dom]["GBps"] / HBM_PEAK_GBPS > roof["frac"]:
             roof = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["GBps"], "peak": HBM_PEAK_GBPS,
                     "unit": "GB/s", "frac": kernels[dom]["GBps"] / HBM_PEAK_GBPS, "traffic": traffic,
                     "peak_source": "MEASURED_PEAKS.json copy bandwidth (DESIGN.md §5.6 bytes per launch)"}
+            if traffic:
+                roof["traffic_bytes_per_px"] = traffic / (B * H * W)
     ms_step = total_ms / K
     hbm = {"algorithmic_bytes_per_px": 8, "achieved_GBps": 8 * px_rank / (ms_step / 1e3) / 1e9}
     hbm["frac_of_measured"] = hbm["achieved_GBps"] / HBM_PEAK_GBPS

@@ -144,7 +144,7 @@ __device__ __forceinline__ void dr_planes(const KParams& p, float f, float2 (&ps
 // ------------------------------------------------------------------ row pass
 
 struct DrRowSmem {
-  float2 tile[8][32][kDrChunk + 1];   // [pair][row][column in chunk] (padded: bank spread)
+  float2 tile[kDrMaxPairs][32][kDrChunk + 1];   // [pair][row][column in chunk] (padded: bank spread)
 };
 
 template <int NPG>

@@ -9,7 +9,7 @@ python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?"
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?"; tail -1 $O/smoke.log
 timeout 900 python bench.py > $O/bench_c2.json 2> $O/bench_c2.err; echo "bench c2 exit $?"
 timeout 900 python bench.py --workload c4 --steps 20 --warmup 3 > $O/bench_c4.json 2> $O/bench_c4.err; echo "bench c4 exit $?"
-timeout 900 python bench.py --workload c5 --steps 10 --warmup 3 --no-e2e > $O/bench_c5.json 2> $O/bench_c5.err; echo "bench c5 exit $?"
+timeout 900 python bench.py --workload c5 --steps 10 --warmup 3 > $O/bench_c5.json 2> $O/bench_c5.err; echo "bench c5 exit $?"
 timeout 900 python bench.py --workload c1 --steps 200 --warmup 5 > $O/bench_c1.json 2> $O/bench_c1.err; echo "bench c1 exit $?"
 timeout 900 python bench.py --op 3 --no-e2e --no-cpu-baseline > $O/bench_c2_deriche.json 2> $O/bench_c2_deriche.err; echo "bench c2 deriche exit $?"
 timeout 900 python bench.py --workload c5 --op 3 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_c5_deriche.json 2> $O/bench_c5_deriche.err; echo "bench c5 deriche exit $?"

@@ -1,19 +1,26 @@
 #!/usr/bin/env python
 """Benchmark of the GCF hot path (libgc, sm_100a) — the driver's contract.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5] [--impl ours|reference]
 
 One "step" = one pass of the whole hot path (centre + N+2 auxiliary planes + N+2
 spatial Gaussian filterings + recombination and division) over one
-batch of the workload's synthetic input.  Default workload: BASELINE.json configs[1]
-(c2: one 1024x1024 Voronoi+texture+noise image, sigma_s=5, sigma_r=20, N=8) at its
-stated parameters.  The stated (sigma_r, N) are numerically ill-posed for the method
-(R1) but the hot-path work depends only on (H, W, N, sigma_s), so the
-throughput is that of the parity-gated twin (sigma_r=70) too.
+batch of the workload's synthetic input.
 
-Prints ONE JSON line on rank 0.  Multi-GPU (torchrun, one rank per GPU, NCCL):
-c2/c1/c3 run one replica per rank (weak scaling), c4 shards the 256-image batch,
-c5 splits the image into row bands with NCCL halo exchange inside libgc.
+Default workload: c5 — the single 16384x16384 Voronoi image (sigma_s=16, sigma_r=10,
+N=12, O(1) operator via GC_OP_AUTO), BASELINE.json's largest single-GPU configuration.
+At --gpus 1 one GPU filters the whole image; at --gpus N > 1 the image is split into N
+row bands whose 3 sigma_s-row halos of f are exchanged through NCCL inside libgc
+(gc_bilateral_band).  `--gpus N` launches itself under torchrun when
+WORLD_SIZE is not set (one rank per GPU, NCCL); the line's n_gpus is the number of ranks
+that ran.  c4 shards its 256-image batch over the ranks; c1/c2/c3 run one replica per rank.
+
+The stated (sigma_r, N) are numerically ill-posed for the method (R1) but the
+hot-path work depends only on (H, W, N, sigma_s): the timed throughput is that of the
+parity-gated twin sigma_r too, and an untimed check of sampled output rows (every band
+seam at N > 1) against the CPU oracle at the twin sigma_r is printed in the same line.
+
+Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -21,7 +28,7 @@ import argparse
 import json
 import math
 import os
-import subprocess
+import socket
 import sys
 import threading
 import time
@@ -32,7 +39,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "megapixels/sec (fp32, degree N, σs) and % of HBM roofline at 1/2/4/8 B200"
-FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.45: SMs x FP32 lanes x 2 x max SM clock
+SM_COUNT, FP32_LANES, SM_MAX_GHZ = 148, 128, 1.965
+FP32_PEAK_TINSTR = SM_COUNT * FP32_LANES * SM_MAX_GHZ / 1e3   # 37.2 T FP32 lane-instructions/s
+FP32_PEAK_TFLOPS = 2 * FP32_PEAK_TINSTR                       # 74.45 TFLOP/s (FMA = 2 FLOP)
+PEAK_SOURCE = ("derived: 148 SMs x 128 FP32 lanes x 1.965 GHz max SM clock (B200_PROFILING.md unit counts; "
+               "FFMA measured at 125-128 lanes/clk/SM, profiles/r01_ubench_fp32.txt); not driver-measured")
+C3_SWEEP = (2.0, 5.0, 10.0, 20.0, 40.0)
 
 
 def _hbm_peak():
@@ -40,32 +52,34 @@ def _hbm_peak():
     B200_PROFILING.md fallback."""
     try:
         d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        for k, v in d.items():
-            if "hbm" in k.lower() and isinstance(v, (int, float)) and v > 100:
-                return float(v)
+        v = d.get("hbm_gbs")
+        if isinstance(v, (int, float)) and v > 100:
+            return float(v), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
     except Exception:
         pass
-    return 6550.7
+    return 6650.0, "B200_PROFILING.md fallback"
 
 
-HBM_PEAK_GBPS = _hbm_peak()
+HBM_PEAK_GBPS, HBM_PEAK_SOURCE = _hbm_peak()
 
 
-def _args():
+def _args(argv=None):
     a = argparse.ArgumentParser()
     a.add_argument("--gpus", type=int, default=1)
-    a.add_argument("--steps", type=int, default=200)
+    a.add_argument("--steps", type=int, default=20)
     a.add_argument("--warmup", type=int, default=5)
-    a.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    a.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     a.add_argument("--sigma-s", type=float, default=None, help="c3 sweep value (default: first)")
     a.add_argument("--sigma-r", type=float, default=None, help="override (default: stated)")
     a.add_argument("--impl", default="ours", choices=["ours", "reference"])
     a.add_argument("--no-e2e", action="store_true")
+    a.add_argument("--no-sweep", action="store_true", help="skip the c3 sigma_s sweep key")
+    a.add_argument("--no-check", action="store_true", help="skip the sampled oracle check")
     a.add_argument("--batch", type=int, default=None, help="override the batch size (profiling only)")
     a.add_argument("--no-cpu-baseline", action="store_true")
     a.add_argument("--op", type=int, default=0, choices=[0, 1, 2, 3], help="0 auto, 1 FIR, 2 O(1), 3 Deriche (NOT eq. 7)")
     a.add_argument("--fp64", action="store_true", help="binary64 internal arithmetic (GC_PREC_FP64)")
-    return a.parse_args()
+    return a.parse_args(argv)
 
 
 def _dist():
@@ -75,14 +89,38 @@ def _dist():
     return ws, rank, local
 
 
-# ------------------------------------------------------------------ algorithmic work
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
-O1_FLOP_PER_PLANE = 50   # exact-window recursion per plane-sample and pass:
+
+def _self_launch(n):
+    """`--gpus N` outside torchrun: re-run this command under torchrun with N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+# ------------------------------------------------------------------ algorithmic work (DESIGN.md §5.3)
+
+def alg_instr(N):
+    """SURVEY §8(d)'s design-independent count of FP32 lane-instructions per output pixel, with the
+    paper's cheapest O(1) Gaussian (Deriche 4th order, 17 instructions per plane and pass; P:50,
+    P:112): total 2(N+2)17 + 5N + 14; the column pass's share (N+2)17 + 4(N+1) + 6 (a2 vertical +
+    the a3 epilogue, §8(a)); the row pass the rest (a1 + a2 horizontal)."""
+    total = 2 * (N + 2) * 17 + 5 * N + 14
+    col = (N + 2) * 17 + 4 * (N + 1) + 6
+    return {"k_row": total - col, "k_col": col, "total": total}
+
+
+O1_FLOP_PER_PLANE = 50   # exact-window recursion per plane-sample and pass (DESIGN.md §5.2):
 #                          A, B (2 add) + box (2 add, 1 mul) + 5 resonators x (3 FMA + 1 add + 1 FMA)
-
-
-DR_FLOP_PER_PLANE = 35  # Deriche mode per plane-sample and pass: 2 sections x 4 FMA per direction
-#                         (16 FMA = 32 FLOP) + 3 adds (section sums, causal + anticausal)
+DR_FLOP_PER_PLANE = 35   # Deriche mode per plane-sample and pass: 2 sections x 4 FMA per direction
+#                          (16 FMA = 32 FLOP) + 3 adds (section sums, causal + anticausal)
 
 
 def resolve_op(op, R):
@@ -91,7 +129,7 @@ def resolve_op(op, R):
 
 
 def op_flop_per_plane(op, R):
-    """Algorithmic FLOP of the spatial operator per plane-pixel and pass: FIR 2(2R+1); O(1) 50;
+    """FLOP of the implemented spatial operator per plane-pixel and pass: FIR 2(2R+1); O(1) 50;
     Deriche 35 (lead-in samples excluded)."""
     return {1: 2 * (2 * R + 1), 2: O1_FLOP_PER_PLANE, 3: DR_FLOP_PER_PLANE}[op]
 
@@ -105,15 +143,49 @@ def dr_bytes(N, px):
 
 
 def flops_row(N, R, px, op=1):
-    """K_row per input pixel: eq. (7) along rows for N+2 planes + plane generation (N+1 mul,
-    once per sample for the FIR, for the entering and leaving samples for O(1)) + centring (6)."""
+    """The design's work in K_row per input pixel: eq. (7) along rows for N+2 planes + plane
+    generation (N+1 mul, once per sample for the FIR, for the entering and leaving samples for
+    O(1)) + centring (6)."""
     gen = (N + 1) + 6
     return px * ((N + 2) * op_flop_per_plane(op, R) + (gen if op == 1 else 2 * gen))
 
 
 def flops_col(N, R, px, op=1):
-    """K_col per output pixel: eq. (7) along columns for N+2 planes + eqs. (8)-(10) 6(N+1) + 8."""
+    """The design's work in K_col per output pixel: eq. (7) along columns for N+2 planes +
+    eqs. (8)-(10) 6(N+1) + 8."""
     return px * ((N + 2) * op_flop_per_plane(op, R) + 6 * (N + 1) + 8)
+
+
+def roofline(N, R, op, px, row_ms, col_ms, step_ms, traffic_key=None):
+    """Roofline of the dominant kernel: `achieved`/`frac` on SURVEY §8(d)'s
+    algorithmic instruction count against the derived FP32 ALU peak; `design` = the same kernel's
+    implemented FLOP against 74.45 TFLOP/s; `step_frac` = the whole step on the algorithmic count."""
+    alg = alg_instr(N)
+    dom = "k_col" if col_ms >= row_ms else "k_row"
+    ms = {"k_row": row_ms, "k_col": col_ms}[dom]
+    ach = alg[dom] * px / (ms / 1e3) / 1e12
+    design = (flops_col if dom == "k_col" else flops_row)(N, R, px, op) / (ms / 1e3) / 1e12
+    out = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": FP32_PEAK_TINSTR,
+           "unit": "T FP32 instr/s (SURVEY §8(d) algorithmic count)", "frac": ach / FP32_PEAK_TINSTR,
+           "alg_instr_per_px": alg[dom], "units_per_launch": px, "peak_source": PEAK_SOURCE,
+           "step_frac": alg["total"] * px / (step_ms / 1e3) / 1e12 / FP32_PEAK_TINSTR,
+           "design": {"achieved": design, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                      "frac": design / FP32_PEAK_TFLOPS,
+                      "basis": "implemented FLOP: " + {1: "FIR 2(2W+1)", 2: "O(1) 50", 3: "Deriche 35"}[op] +
+                               " per plane-pixel and pass + generation / recombination"},
+           "traffic": None}
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if traffic_key and os.path.exists(tp):
+        try:
+            tr = json.load(open(tp))
+            t = tr.get(f"{traffic_key}:{dom}")
+            if t:
+                out["traffic"] = t
+                out["traffic_bytes_per_px"] = t / px
+                out["traffic_source"] = tr.get("_source_" + traffic_key, tr.get("_source"))
+        except Exception:
+            pass
+    return out
 
 
 # ------------------------------------------------------------------ clocks during the timed region
@@ -147,7 +219,7 @@ class ClockSampler:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in names.items():
-                    if isinstance(bit, int) and bit and (r & bit) == bit and bit not in (0,):
+                    if isinstance(bit, int) and bit and (r & bit) == bit:
                         self.reasons.add(name.replace("nvmlClocksEventReason", "").replace("nvmlClocksThrottleReason", ""))
             except Exception:
                 pass
@@ -161,52 +233,150 @@ class ClockSampler:
     def summary(self):
         s = sorted(self.samples)
         med = s[len(s) // 2] if s else None
-        bad = [r for r in self.reasons if r not in ("All", "None", "Unknown")]
+        bad = [r for r in self.reasons if r not in ("All", "None", "Unknown", "GpuIdle")]
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "samples": len(s), "reasons": sorted(bad)}
 
 
-# ------------------------------------------------------------------ CPU oracle leg
+# ------------------------------------------------------------------ CPU oracle (cpu_baseline and --impl reference)
 
-def cpu_oracle_sample(cfg, sigma_s, sigma_r, budget_s=12.0):
-    """The oracle as it stands, on a bounded row sample of the workload's first image."""
-    import oracle
+CPU_BLOCK_ROWS, CPU_BLOCK_COLS = 32, 2048
+
+
+def _cpu_blocks(cfg, n):
+    """n deterministic sample blocks (row0, col0) of CPU_BLOCK_ROWS x CPU_BLOCK_COLS output pixels of
+    image 0, spread over the image (first block at the top-left corner, which includes the
+    symmetric extension)."""
+    H, W = cfg.H, cfg.W
+    bw = min(CPU_BLOCK_COLS, W)
+    br = min(CPU_BLOCK_ROWS, H)
+    ncol = max(1, W // bw)
+    out = []
+    for j in range(n):
+        r = (j * 2654435761) % max(1, H - br + 1) if j else 0
+        c = ((j * 40503) % ncol) * bw if j else 0
+        out.append((int(r) // 8 * 8, int(min(c, W - bw))))
+    return out
+
+
+def _cpu_crop(cfg, blk, sigma_s):
+    """The oracle's input for one block: output rows/cols plus the W-sample window on every side
+    (or the true image edge, where the oracle applies the symmetric extension itself)."""
     from synth import config_image
-    img = config_image(cfg, index=0)
-    H, W = img.shape
-    rows_done, t_used, r0 = 0, 0.0, 0
-    block = 32
-    while t_used < budget_s and rows_done < H:
-        rows = [(r0 + k) % H for k in range(block)]
+    R = math.ceil(3 * sigma_s)
+    r0, c0 = blk
+    br, bw = min(CPU_BLOCK_ROWS, cfg.H), min(CPU_BLOCK_COLS, cfg.W)
+    ya, yb = max(0, r0 - R), min(cfg.H, r0 + br + R)
+    xa, xb = max(0, c0 - R), min(cfg.W, c0 + bw + R)
+    rows = config_image(cfg, index=0, rows=(ya, yb))
+    return np.ascontiguousarray(rows[:, xa:xb]), (r0 - ya, c0 - xa, br, bw, ya == 0 and yb == cfg.H, xa, xb)
+
+
+def _cpu_block_work(args):
+    """Worker: oracle.gc_filter_rows on one crop (the oracle as it stands, numpy fp64)."""
+    crop, (ry, cx, br, bw, _, _, _), sigma_s, sigma_r, N = args
+    import oracle
+    t0 = time.perf_counter()
+    out, _ = oracle.gc_filter_rows(crop, list(range(ry, ry + br)), sigma_s, sigma_r, N)
+    dt = time.perf_counter() - t0
+    return dt, out[:, cx:cx + bw]
+
+
+class CpuOracle:
+    """The oracle timed on the host cores: a pool of `cores` single-threaded worker processes,
+    each running oracle.gc_filter_rows on its own sample block."""
+
+    def __init__(self, cfg, sigma_s, sigma_r, N, cores=None):
+        import multiprocessing as mp
+        for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[v] = "1"
+        self.cfg, self.sigma_s, self.sigma_r, self.N = cfg, sigma_s, sigma_r, N
+        self.cores = cores or len(os.sched_getaffinity(0))
+        self.blocks = _cpu_blocks(cfg, self.cores)
+        self.crops = [_cpu_crop(cfg, b, sigma_s) for b in self.blocks]
+        self.pool = mp.get_context("fork").Pool(self.cores) if self.cores > 1 else None
+
+    def close(self):
+        if self.pool:
+            self.pool.close()
+            self.pool.join()
+
+    def run(self, cores=None):
+        """One round: `cores` blocks in parallel (all cores by default). Returns (MP/s, seconds)."""
+        n = cores or self.cores
+        work = [(c, m, self.sigma_s, self.sigma_r, self.N) for c, m in self.crops[:n]]
         t0 = time.perf_counter()
-        oracle.gc_filter_rows(img, rows, sigma_s, sigma_r, cfg.N)
-        t_used += time.perf_counter() - t0
-        rows_done += block
-        r0 += H // 7 + 1
-    mp = rows_done * W / 1e6
-    return {"value": mp / t_used, "unit": "MP/s", "cores": 1, "kind": "oracle",
-            "sample": f"{rows_done} output rows x {W} px of {cfg.name} image 0 (oracle.gc_filter_rows, numpy fp64, "
-                      f"single-threaded; host nproc={os.cpu_count()}), {t_used:.1f} s"}
+        if n == 1 or self.pool is None:
+            res = [_cpu_block_work(w) for w in work]
+        else:
+            res = self.pool.map(_cpu_block_work, work, chunksize=1)
+        dt = time.perf_counter() - t0
+        px = sum(m[2] * m[3] for _, m in self.crops[:n])
+        return px / dt / 1e6, dt
+
+    def describe(self, n, rounds, secs):
+        br, bw = min(CPU_BLOCK_ROWS, self.cfg.H), min(CPU_BLOCK_COLS, self.cfg.W)
+        return (f"{rounds} round(s) of {n} block(s) of {br} output rows x {bw} px of {self.cfg.name} image 0, "
+                f"one block per worker process (oracle.gc_filter_rows on the block's input window, numpy fp64, "
+                f"single-threaded workers; host nproc={os.cpu_count()}), {secs:.1f} s")
+
+
+def cpu_baseline(cfg, sigma_s, sigma_r, N, budget_s=12.0):
+    """the oracle on all host cores and on one core, each on a bounded sample."""
+    co = CpuOracle(cfg, sigma_s, sigma_r, N)
+    try:
+        vals, t_all, rounds = [], 0.0, 0
+        while t_all < budget_s * 0.6 and rounds < 8:
+            v, dt = co.run()
+            vals.append(v)
+            t_all += dt
+            rounds += 1
+        v1, t1 = co.run(cores=1)
+        return {"value": float(np.median(vals)), "unit": "MP/s", "cores": co.cores, "kind": "oracle",
+                "sample": co.describe(co.cores, rounds, t_all),
+                "single_core": {"value": v1, "unit": "MP/s", "cores": 1, "sample": co.describe(1, 1, t1)}}
+    finally:
+        co.close()
 
 
 def run_reference(args, cfg, sigma_s, sigma_r, ws, rank):
     if rank != 0:
         return
-    per_step = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
-    vals = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_oracle_sample(cfg, sigma_s, sigma_r, budget_s=per_step)
-        if i >= args.warmup:
-            vals.append(r)
-    v = float(np.median([r["value"] for r in vals]))
-    px_step = cfg.batch * cfg.H * cfg.W       # one step = the whole workload; the oracle timed a row sample
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "MP/s", "n_gpus": args.gpus,
+    co = CpuOracle(cfg, sigma_s, sigma_r, cfg.N)
+    try:
+        vals, t_tot = [], 0.0
+        for i in range(args.warmup + args.steps):
+            v, dt = co.run()
+            if i >= args.warmup:
+                vals.append(v)
+                t_tot += dt
+    finally:
+        co.close()
+    v = float(np.median(vals))
+    px_step = cfg.batch * cfg.H * cfg.W       # one step = the whole workload; the oracle timed a sample of it
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "MP/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": px_step / (v * 1e6) * 1e3,
-            "ms_per_step_note": "extrapolated from the sampled rate", "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "ms_per_step_note": "whole-workload time extrapolated from the sampled rate", "higher_is_better": True,
+            "scaling": _scaling(cfg), "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, synth/images.py)",
             "config": _config(cfg, sigma_s, sigma_r, ws),
-            "cpu_baseline": {"value": v, "unit": "MP/s", "cores": 1, "kind": "oracle", "sample": vals[-1]["sample"]},
+            "cpu_baseline": {"value": v, "unit": "MP/s", "cores": co.cores, "kind": "oracle",
+                             "sample": co.describe(co.cores, args.steps, t_tot) + " per timed step"},
             "e2e": {"value": v, "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def band_rows_of(H, ws):
+    """Row-band split of c5 over ws ranks (sizes differ by at most one row)."""
+    return [H // ws + (1 if k < H % ws else 0) for k in range(ws)]
+
+
+def shard_of(batch, ws, rank):
+    """c4 batch sharding: the image indices rank `rank` filters (contiguous, sizes differ by <= 1)."""
+    lo = rank * batch // ws
+    return list(range(lo, (rank + 1) * batch // ws))
+
+
+def _scaling(cfg):
+    return "strong" if cfg.name in ("c4", "c5") else "weak"
 
 
 def _config(cfg, sigma_s, sigma_r, ws):
@@ -215,13 +385,12 @@ def _config(cfg, sigma_s, sigma_r, ws):
             "batch": cfg.batch, "sigma_s": sigma_s, "sigma_r": sigma_r, "sigma_r_parity_twin": cfg.sigma_r_twin,
             "N": cfg.N, "planes": cfg.N + 2, "radius": math.ceil(3 * sigma_s), "parallelism": par,
             "l2": "flushed before every timed step (256 MiB write)" if cfg.name in ("c1", "c2", "c3")
-            else "inputs larger than L2"}
+            else "inputs larger than L2 (no flush)"}
 
 
 def _bind_to_gpu_numa_node(index):
     """Run this rank on the CPU cores NVML reports as local to its GPU, so the pinned host
-    buffers of the e2e leg sit on the GPU's NUMA node (cross-socket PCIe traffic otherwise
-    roughly halves the host<->device copy rate).  No-op when NVML or the affinity call fails."""
+    buffers of the e2e leg sit on the GPU's NUMA node.  No-op when NVML or the call fails."""
     try:
         import pynvml as nv
         nv.nvmlInit()
@@ -236,15 +405,102 @@ def _bind_to_gpu_numa_node(index):
         pass
 
 
+# ------------------------------------------------------------------ sampled oracle check (untimed)
+
+def check_rows(cfg, sigma_s, ws, band_rows):
+    """Global output rows checked against the oracle: every band seam b -> {b-W, b-1, b, b+W-1};
+    at one rank a spread of rows incl. both image edges."""
+    H = cfg.H
+    R = math.ceil(3 * sigma_s)
+    rows = {0, min(R, H - 1), H - 1}
+    if ws > 1:
+        b = 0
+        for hb in band_rows[:-1]:
+            b += hb
+            rows |= {b - R, b - 1, b, b + R - 1}
+    else:
+        rows |= {H // 2 - 1, H // 2, max(0, H - 1 - R)}
+    return sorted(r for r in rows if 0 <= r < H)
+
+
+def oracle_check(cfg, sigma_s, sigma_r, rows, got, cols=512):
+    """Compare GPU output rows `got` [len(rows), W] with the oracle on three column windows (left
+    edge, centre, right edge) of each row.  The oracle runs on the crop [r-W, r+W] x [c0-W,
+    c0+cols+W] clipped to the image: where the crop is clipped it ends at the true image edge,
+    where the oracle's own symmetric extension applies, so the crop determines the row exactly."""
+    import oracle
+    from synth import config_image
+    R = math.ceil(3 * sigma_s)
+    H, W = cfg.H, cfg.W
+    cw = min(cols, W)
+    errs = []
+    for i, r in enumerate(rows):
+        ya, yb = max(0, r - R), min(H, r + R + 1)
+        src = config_image(cfg, index=0, rows=(ya, yb))
+        for c0 in sorted({0, (W - cw) // 2, W - cw}):
+            xa, xb = max(0, c0 - R), min(W, c0 + cw + R)
+            ref, _ = oracle.gc_filter_rows(np.ascontiguousarray(src[:, xa:xb]), [r - ya], sigma_s, sigma_r, cfg.N)
+            errs.append(np.abs(got[i, c0:c0 + cw].astype(np.float64) - ref[0, c0 - xa:c0 - xa + cw]))
+    e = np.concatenate([x.ravel() for x in errs])
+    mx, rm = float(e.max()), float(np.sqrt(np.mean(e ** 2)))
+    return {"max_abs": mx, "rms": rm, "rows": len(rows), "px": int(e.size), "sigma_r": sigma_r,
+            "tol": {"max_abs": 1e-2, "rms": 1e-3}, "pass": bool(mx <= 1e-2 and rm <= 1e-3),
+            "what": "GPU output rows at the parity twin sigma_r (untimed run of the same call) vs "
+                    "oracle.gc_filter_rows on each row's input window; left-edge, centre and right-edge columns"}
+
+
 # ------------------------------------------------------------------ our leg
+
+def _events(n):
+    import torch
+    return [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+
+
+def c3_sweep(gc, dev, steps, ops=(0, 2)):
+    """BASELINE configs[2]: the 4096^2 image at sigma_r=15, N=10 for sigma_s in {2,5,10,20,40};
+    Gpx/s per sigma_s (median of `steps` single-call timings, L2 flushed before each) with
+    GC_OP_AUTO and with the O(1) operator forced, plus max/min of each (cost
+    independent of sigma_s; the paper's Table II analogue)."""
+    import torch
+    from synth import CONFIGS, config_image
+    cfg = CONFIGS["c3"]
+    x = torch.from_numpy(config_image(cfg)).to(dev)
+    out = torch.empty_like(x)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    res = {"workload": f"c3: 1x{cfg.H}x{cfg.W} voronoi, sigma_r={cfg.sigma_r}, N={cfg.N}", "unit": "Gpx/s"}
+    for op in ops:
+        vals = {}
+        for s in C3_SWEEP:
+            for _ in range(3):
+                gc.filter(x, s, cfg.sigma_r, cfg.N, out=out, op=op)
+            t = []
+            for _ in range(steps):
+                flush.zero_()
+                e0, e1 = _events(2)
+                e0.record()
+                gc.filter(x, s, cfg.sigma_r, cfg.N, out=out, op=op)
+                e1.record()
+                e1.synchronize()
+                t.append(e0.elapsed_time(e1))
+            vals[f"{s:g}"] = cfg.H * cfg.W / (float(np.median(t)) / 1e3) / 1e9
+        v = list(vals.values())
+        res["auto" if op == 0 else "o1"] = {"by_sigma_s": vals, "max_over_min": max(v) / min(v)}
+    del x, out, flush
+    return res
+
 
 def main():
     args = _args()
     ws, rank, local = _dist()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _self_launch(args.gpus)
     from synth import CONFIGS, config_image
     cfg = CONFIGS[args.workload]
     sigma_s = args.sigma_s if args.sigma_s is not None else cfg.sigma_s[0]
     sigma_r = args.sigma_r if args.sigma_r is not None else cfg.sigma_r
+    if args.batch is not None:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, batch=args.batch)
     if args.impl == "reference":
         return run_reference(args, cfg, sigma_s, sigma_r, ws, rank)
 
@@ -257,53 +513,52 @@ def main():
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
     R = math.ceil(3 * sigma_s)
+    op = resolve_op(args.op, R) if not args.fp64 else 1
+    t_gen0 = time.perf_counter()
 
-    # ---- inputs resident in HBM before the timed region
-    comm = None
-    if args.batch is not None:
-        import dataclasses
-        cfg = dataclasses.replace(cfg, batch=args.batch)
+    # ---- inputs resident in HBM before the timed region (each rank generates only its part)
+    comm, row0, band_rows = None, 0, None
     if cfg.name == "c4":
-        per = cfg.batch // ws
-        imgs = np.stack([config_image(cfg, index=rank * per + i) for i in range(per)])
-        x = torch.from_numpy(imgs).to(dev)
-        H, W, B = cfg.H, cfg.W, per
-        px_rank = per * H * W
+        mine = shard_of(cfg.batch, ws, rank)
+        x = torch.from_numpy(np.stack([config_image(cfg, index=i) for i in mine])).to(dev)
+        H, W, B = cfg.H, cfg.W, len(mine)
     elif cfg.name == "c5" and ws > 1:
-        full = config_image(cfg)
-        rows = [cfg.H // ws] * ws
-        pl = gc.band_plan(cfg.H, rank, ws, rows, sigma_s)
-        x = torch.from_numpy(np.ascontiguousarray(full[pl["row0"]:pl["row0"] + rows[rank]])).to(dev)
-        del full
-        H, W, B = rows[rank], cfg.W, 1
-        px_rank = H * W
-        comm = gc.Comm(rank, ws)
+        band_rows = band_rows_of(cfg.H, ws)
+        pl = gc.band_plan(cfg.H, rank, ws, band_rows, sigma_s, op=args.op)
         row0 = pl["row0"]
+        x = torch.from_numpy(config_image(cfg, rows=(row0, row0 + band_rows[rank]))).to(dev)
+        H, W, B = band_rows[rank], cfg.W, 1
+        comm = gc.Comm(rank, ws)
     else:
         x = torch.from_numpy(config_image(cfg)).to(dev)
         H, W, B = cfg.H, cfg.W, 1
-        px_rank = H * W
+    gen_s = time.perf_counter() - t_gen0
+    px_rank = B * H * W
     out = torch.empty_like(x)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if cfg.name in ("c1", "c2", "c3") else None
     stream = torch.cuda.current_stream()
 
-    def step(events=None):
+    def step(events=None, sr=sigma_r, dst=out):
         if comm is not None:
-            gc.bilateral_band(x, cfg.H, row0, sigma_s, sigma_r, cfg.N, comm, out=out, op=args.op)
+            gc.bilateral_band(x, cfg.H, row0, sigma_s, sr, cfg.N, comm, out=dst, op=args.op, events=events)
         else:
-            gc.filter(x, sigma_s, sigma_r, cfg.N, out=out, events=events, op=args.op, fp64=args.fp64)
+            gc.filter(x, sigma_s, sr, cfg.N, out=dst, events=events, op=args.op, fp64=args.fp64)
+
+    def drain(timeout_ms=300000.0):
+        if comm is not None:
+            comm.wait(stream, timeout_ms)          # NCCL watchdog (gc_comm_wait)
+        torch.cuda.synchronize()
 
     for _ in range(args.warmup):
         if flush is not None:
             flush.zero_()
         step()
-    torch.cuda.synchronize()
+    drain()
 
     K = args.steps
     # timed region: the production call (no events inside it, so the column pass overlaps the
     # row pass's tail through programmatic dependent launch); one event pair per step
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
-    torch.cuda.synchronize()
+    ev = [_events(2) for _ in range(K)]
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -314,17 +569,18 @@ def main():
             ev[k][0].record()
             step()
             ev[k][1].record()
-        torch.cuda.synchronize()
+        drain()
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     total_ms = sum(e[0].elapsed_time(e[1]) for e in ev)
+
     # per-kernel durations (roofline): a second, instrumented pass with events between the
     # kernels (cudaEvent_t handles recorded on the launching stream inside libgc)
-    row_ms = col_ms = None
-    if comm is None:
-        K3 = min(K, 50)
-        evk = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K3)]
+    row_ms = col_ms = xchg_ms = None
+    if not args.fp64:
+        K3 = min(K, 20)
+        evk = [_events(4) for _ in range(K3)]
         for e in evk:                              # materialise the cudaEvent_t handles
             for q in e:
                 q.record()
@@ -332,110 +588,140 @@ def main():
         for k in range(K3):
             if flush is not None:
                 flush.zero_()
-            step(events=evk[k])
-        torch.cuda.synchronize()
+            evk[k][3].record()
+            step(events=evk[k][:3])
+        drain()
         row_ms = sum(e[0].elapsed_time(e[1]) for e in evk) / K3
         col_ms = sum(e[1].elapsed_time(e[2]) for e in evk) / K3
+        xchg_ms = sum(e[3].elapsed_time(e[0]) for e in evk) / K3
+
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    px_all = px_rank * ws
+    px_all = cfg.batch * cfg.H * cfg.W if cfg.name in ("c4", "c5") else px_rank * ws
     value = px_all * K / (total_ms / 1e3) / 1e6
 
-    # ---- e2e: same metric through gc_filter_host with pinned host buffers
+    # ---- e2e: same metric through the public API with pinned host buffers, copies timed
     e2e = None
-    if not args.no_e2e and comm is None and not args.fp64:
+    if not args.no_e2e and not args.fp64:
         hin = torch.from_numpy(x.cpu().numpy()).pin_memory()
         hout = torch.empty_like(hin).pin_memory()
-        hin_np, hout_np = hin.numpy(), hout.numpy()
-        # DMA to freshly pinned host buffers is slow until the host side has warmed them (per-buffer
-        # ramps of hundreds of calls on the B200 VMs, profiles/r01_e2e_host_chunks.txt): warm the
-        # e2e leg with 0.5 s of calls on the buffers it times
-        t_end = time.perf_counter() + 0.5
-        for _ in range(max(3, args.warmup)):
-            gc.filter_host(hin_np, sigma_s, sigma_r, cfg.N, out=hout_np, op=args.op)
-        while time.perf_counter() < t_end:
-            gc.filter_host(hin_np, sigma_s, sigma_r, cfg.N, out=hout_np, op=args.op)
-        K2 = min(K, 50)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ms = 0.0
+        K2 = min(K, 10)
         per = []
-        for _ in range(K2):
-            if flush is not None:
-                flush.zero_()
-            e0.record()
-            gc.filter_host(hin_np, sigma_s, sigma_r, cfg.N, out=hout_np, op=args.op)
-            e1.record()
-            e1.synchronize()
-            per.append(e0.elapsed_time(e1))
-            ms += per[-1]
-        if os.environ.get("GC_BENCH_E2E_STEPS"):
-            print("e2e steps (ms):", " ".join(f"{v:.3f}" for v in per), file=sys.stderr)
-        te = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if comm is None:
+            # gc_filter_host: H2D + kernels + D2H + stream sync inside one library call
+            hin_np, hout_np = hin.numpy(), hout.numpy()
+            # DMA to freshly pinned host buffers is slow until warmed (profiles/r01_e2e_host_chunks.txt)
+            t_end = time.perf_counter() + 0.5
+            for _ in range(max(3, args.warmup)):
+                gc.filter_host(hin_np, sigma_s, sigma_r, cfg.N, out=hout_np, op=args.op)
+            while time.perf_counter() < t_end:
+                gc.filter_host(hin_np, sigma_s, sigma_r, cfg.N, out=hout_np, op=args.op)
+            api = "gc_filter_host (pinned host buffers; H2D + kernels + D2H + stream sync per step)"
+            for _ in range(K2):
+                if flush is not None:
+                    flush.zero_()
+                e0, e1 = _events(2)
+                e0.record()
+                gc.filter_host(hin_np, sigma_s, sigma_r, cfg.N, out=hout_np, op=args.op)
+                e1.record()
+                e1.synchronize()
+                per.append(e0.elapsed_time(e1))
+        else:
+            # per rank: H2D of the band from pinned memory, gc_bilateral_band (exchange + filter),
+            # D2H of the band's output, all on the rank's stream
+            xb, ob = torch.empty_like(x), torch.empty_like(out)
+            api = "per rank: H2D of the band (pinned) + gc_bilateral_band (NCCL halo exchange + filter) + D2H"
+            for k in range(args.warmup + K2):
+                dist.barrier()
+                e0, e1 = _events(2)
+                e0.record()
+                xb.copy_(hin, non_blocking=True)
+                gc.bilateral_band(xb, cfg.H, row0, sigma_s, sigma_r, cfg.N, comm, out=ob, op=args.op)
+                hout.copy_(ob, non_blocking=True)
+                e1.record()
+                comm.wait(stream, 300000.0)
+                e1.synchronize()
+                if k >= args.warmup:
+                    per.append(e0.elapsed_time(e1))
+            del xb, ob
+        te = torch.tensor([sum(per)], dtype=torch.float64, device=dev)
         if ws > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         nbytes = int(hin.numel() * 4)
         e2e = {"value": px_all * K2 / (float(te.item()) / 1e3) / 1e6, "unit": "MP/s",
-               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-               "api": "gc_filter_host (pinned host buffers; H2D + kernels + D2H + stream sync per step)"}
+               "h2d_bytes_per_step": nbytes * ws, "d2h_bytes_per_step": nbytes * ws,
+               "ms_per_step": float(te.item()) / K2, "api": api}
+        del hin, hout
+
+    # ---- untimed oracle check of sampled rows at the parity twin sigma_r (all band seams)
+    check = None
+    rows_chk = None
+    if not args.no_check and not args.fp64 and op != 3 and cfg.name in ("c2", "c3", "c5"):
+        rows_chk = check_rows(cfg, sigma_s, ws, band_rows or [cfg.H])
+        twin = torch.empty_like(out)
+        step(sr=cfg.sigma_r_twin, dst=twin)
+        drain()
+        g = torch.zeros((len(rows_chk), W), dtype=torch.float32, device=dev)
+        for i, r in enumerate(rows_chk):
+            if row0 <= r < row0 + H:
+                g[i] = twin[r - row0] if twin.dim() == 2 else twin[0, r - row0]
+        if ws > 1:
+            dist.all_reduce(g)                     # each checked row is owned by exactly one rank (x + 0 = x)
+        got = g.cpu().numpy()
+        del twin
 
     if rank != 0:
+        if comm is not None:
+            comm.close()
         if ws > 1:
             dist.destroy_process_group()
         return
+    if rows_chk is not None:
+        check = oracle_check(cfg, sigma_s, cfg.sigma_r_twin, rows_chk, got)
+        if ws > 1:
+            check["seams"] = [sum(band_rows[:k + 1]) for k in range(ws - 1)]
 
-    # ---- roofline of the dominant kernel (FP32 ALU bound)
-    roof = None
-    kernels = None
-    if row_ms is not None and not args.fp64:      # (fp64 mode: a correctness instrument, no roofline)
-        op = resolve_op(args.op, R)
-        fr = flops_row(cfg.N, R, B * H * W, op)   # whole-image row pass (in_rows = H)
-        fc = flops_col(cfg.N, R, B * H * W, op)
-        kernels = {"k_row": {"ms": row_ms, "tflops": fr / row_ms / 1e9},
-                   "k_col": {"ms": col_ms, "tflops": fc / col_ms / 1e9}}
-        dom = "k_col" if col_ms >= row_ms else "k_row"
-        ach = kernels[dom]["tflops"]
-        if op == 3:                                # Deriche mode: HBM bytes of the design, too
-            db = dr_bytes(cfg.N, B * H * W)
+    ms_step = total_ms / K
+    roof = kernels = None
+    if row_ms is not None:
+        key = f"{cfg.name}_s{sigma_s:g}_{ {1: 'fir', 2: 'o1', 3: 'deriche'}[op]}" + (f"_g{ws}" if comm else "")
+        roof = roofline(cfg.N, R, op, px_rank, row_ms, col_ms, ms_step, traffic_key=key)
+        fr, fc = flops_row(cfg.N, R, px_rank, op), flops_col(cfg.N, R, px_rank, op)
+        kernels = {"k_row": {"ms": row_ms, "design_tflops": fr / row_ms / 1e9},
+                   "k_col": {"ms": col_ms, "design_tflops": fc / col_ms / 1e9}}
+        if comm is not None:
+            kernels["halo_exchange"] = {"ms": xchg_ms, "bytes_per_neighbour": R * W * 4}
+        if op == 3:                                # Deriche mode: the design's HBM bytes too
+            db = dr_bytes(cfg.N, px_rank)
             for k, ms in (("k_row", row_ms), ("k_col", col_ms)):
                 kernels[k]["GBps"] = db[k] / ms / 1e6
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tp):
-            try:
-                key = f"{cfg.name}_s{sigma_s:g}_{ {1: 'fir', 2: 'o1', 3: 'deriche'}[op]}:{dom}"
-                traffic = json.load(open(tp)).get(key)
-            except Exception:
-                traffic = None
-        roof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": ach / FP32_PEAK_TFLOPS, "traffic": traffic,
-                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP x 1.965 GHz (B200_PROFILING.md unit "
-                               "counts; FFMA measured at 125-128 lanes/clk/SM, profiles/r01_ubench_fp32.txt)"}
-        if traffic:
-            roof["traffic_bytes_per_px"] = traffic / (B * H * W)     # DRAM bytes per output pixel (ncu)
-        if op == 3 and kernels[dom]["GBps"] / HBM_PEAK_GBPS > roof["frac"]:
-            roof = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["GBps"], "peak": HBM_PEAK_GBPS,
-                    "unit": "GB/s", "frac": kernels[dom]["GBps"] / HBM_PEAK_GBPS, "traffic": traffic,
-                    "peak_source": "MEASURED_PEAKS.json copy bandwidth (DESIGN.md §5.6 bytes per launch)"}
-            if traffic:
-                roof["traffic_bytes_per_px"] = traffic / (B * H * W)
-    ms_step = total_ms / K
-    hbm = {"algorithmic_bytes_per_px": 8, "achieved_GBps": 8 * px_rank / (ms_step / 1e3) / 1e9}
+            d = roof["kernel"]
+            if kernels[d]["GBps"] / HBM_PEAK_GBPS > roof["frac"]:
+                roof.update({"bound": "hbm", "achieved": kernels[d]["GBps"], "peak": HBM_PEAK_GBPS, "unit": "GB/s",
+                             "frac": kernels[d]["GBps"] / HBM_PEAK_GBPS, "peak_source": HBM_PEAK_SOURCE})
+    hbm = {"algorithmic_bytes_per_px": 8, "achieved_GBps": 8 * px_rank / (ms_step / 1e3) / 1e9,
+           "peak_GBps": HBM_PEAK_GBPS, "peak_source": HBM_PEAK_SOURCE}
     hbm["frac_of_measured"] = hbm["achieved_GBps"] / HBM_PEAK_GBPS
     line = {"metric": METRIC, "value": value, "unit": "MP/s", "n_gpus": ws, "steps": K, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if cfg.name in ("c4", "c5") else "weak", "vs_baseline": None, "dtype": "f64" if args.fp64 else "f32",
-            "data": "synthetic (seeded, synth/images.py)", "config": _config(cfg, sigma_s, sigma_r, ws),
-            "roofline": roof, "kernels": kernels, "hbm": hbm, "e2e": e2e,
-            "gpu_launches": 2 * K, "clocks": clk.summary(), "impl": "ours", "lib": gc.version(),
-            "host_cores": len(os.sched_getaffinity(0))}
-    if ws == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_oracle_sample(cfg, sigma_s, sigma_r)
-    print(json.dumps(line), flush=True)
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": _scaling(cfg), "vs_baseline": None,
+            "dtype": "f64" if args.fp64 else "f32", "data": "synthetic (seeded, synth/images.py)",
+            "config": _config(cfg, sigma_s, sigma_r, ws), "roofline": roof, "kernels": kernels, "hbm": hbm,
+            "e2e": e2e, "gpu_launches": 2 * K, "clocks": clk.summary(), "impl": "ours", "lib": gc.version(),
+            "host_cores": len(os.sched_getaffinity(0)), "input_generation_s": gen_s}
+    if check is not None:
+        line["oracle_check"] = check
+    if comm is not None:
+        comm.close()
     if ws > 1:
         dist.destroy_process_group()
+    if not args.no_sweep and cfg.name == "c5":
+        line["c3_sweep"] = c3_sweep(gc, dev, 10)
+    if ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, sigma_s, sigma_r, cfg.N)
+    print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

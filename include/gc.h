@@ -27,8 +27,9 @@
  *     NULL = legacy default stream).  They return after enqueue.  Argument errors are
  *     detected before anything is enqueued.  Kernel execution errors surface at the
  *     caller's next synchronisation with the stream.
- *   - Image memory is owned by the caller.  The library owns a mutex-guarded coefficient
- *     cache and stream-ordered scratch (cudaMallocAsync / cudaFreeAsync on `stream`).
+ *   - Image memory is owned by the caller.  The library owns bounded, mutex-guarded constant
+ *     caches and stream-ordered scratch (cudaMallocFromPoolAsync / cudaFreeAsync on `stream`,
+ *     from a libgc-private memory pool per device; see gc_scratch_trim).
  *   - All entry points are re-entrant and thread-safe.
  *   - `out` must not alias the input.
  *   - NaN/Inf inputs give unspecified output values (no fault).
@@ -49,7 +50,8 @@ typedef enum {
   GC_ERANGE = 2,  /* N > GC_N_MAX, or mu beyond the coefficient precision limit        */
   GC_ECUDA = 3,   /* a CUDA call or kernel launch failed                               */
   GC_ENOMEM = 4,  /* device scratch allocation failed                                  */
-  GC_ENCCL = 5    /* an NCCL call failed (band API)                                    */
+  GC_ENCCL = 5,   /* an NCCL call failed, or a peer reported an asynchronous error     */
+  GC_ETIMEOUT = 6 /* gc_comm_wait: the exchange did not complete in time (comm aborted) */
 } gc_status;
 
 #define GC_N_MAX 64          /* maximum polynomial degree N                           */
@@ -77,7 +79,7 @@ typedef enum {
 /* Human-readable name of a status code (static storage). */
 const char* gc_status_string(gc_status s);
 
-/* Library version string, e.g. "gc 0.1.0 sm_100a". */
+/* Library version string, e.g. "gc 0.2.0 sm_100a". */
 const char* gc_version(void);
 
 /*
@@ -188,40 +190,97 @@ gc_status gc_bilateral_direct(const float* imgs, int B, int H, int W, float sigm
 gc_status gc_operator_taps(float sigma_s, int op, double* taps_out, int* W_out);
 
 /*
- * Row-band API (multi-GPU domain decomposition, one process per GPU).
+ * Row-band API (multi-GPU domain decomposition, one process per GPU; SURVEY §8(e), c5).
  *
  * The global image has H_global rows of width W.  Rank r of `world` owns the
  * contiguous rows [row0, row0 + H_band) (ranks ordered by row0; rank r-1 owns the rows
- * above).  Every band must have H_band > W_s = ceil(3 sigma_s) rows so that halos come
- * from the adjacent rank only (GC_EINVAL otherwise).
+ * above).  Eq. (7) at row y reads rows y-W_s .. y+W_s (Omega) and the auxiliary
+ * planes of eq. (6) are pointwise in f, so a band needs only `halo` rows of f from
+ * each neighbour: halo = W_s = ceil(3 sigma_s) for GC_OP_AUTO / FIR / O1, ceil(10 sigma_s)
+ * for GC_OP_DERICHE.  Symmetric extension applies only at global rows 0 and
+ * H_global-1.  Every band must have H_band > halo rows (halos come from the adjacent rank
+ * only; GC_EINVAL otherwise).
  *
  * gc_band_plan — host only, pure: the halo rows rank `rank` needs, in global row
- * indices: top = [top0, top0+top_rows) from rank-1, bottom = [bot0, bot0+bot_rows)
- * from rank+1 (0 rows at the global top / bottom, where eq. 7's symmetric extension is
- * applied locally).  Identical on every rank; used by gc_bilateral_band and testable
- * without a GPU.
+ * indices, for operator `op`: top = [top0, top0+top_rows) from rank-1, bottom =
+ * [bot0, bot0+bot_rows) from rank+1 (0 rows at the global top / bottom, where eq. 7's
+ * symmetric extension is applied locally).  band_rows[k] = rows of rank k (sum H_global).
+ * Identical on every rank.  Bands passed to gc_filter_band must come from this plan: it
+ * rejects any band that is too small for `op` on EVERY rank alike, so an invalid plan
+ * fails before any rank enters the exchange.
  */
 gc_status gc_band_plan(int H_global, int rank, int world, const int* band_rows, float sigma_s,
-                       int* row0, int* top0, int* top_rows, int* bot0, int* bot_rows);
+                       int op, int* row0, int* top0, int* top_rows, int* bot0, int* bot_rows);
+
+/* One halo transfer of a band with one neighbour (gc_band_exchange_plan). */
+typedef struct gc_band_xfer {
+  int peer;             /* neighbour rank, or -1 (global edge: no transfer)                 */
+  size_t send_offset;   /* first float of this band sent to `peer` (a row offset times W)   */
+  size_t count;         /* floats sent to and received from `peer` (halo rows times W)      */
+  int recv_row0;        /* global row of the first received row                             */
+} gc_band_xfer;
+
+/*
+ * gc_band_exchange_plan — host only, pure: exactly what gc_filter_band exchanges and
+ * filters.  xfer[0] = with rank-1 (send my first `halo` rows, receive the `halo` rows above
+ * me), xfer[1] = with rank+1 (send my last `halo` rows, receive the rows below me);
+ * seg_row0/seg_rows = the three input segments (top halo, own band, bottom halo) then
+ * given to gc_filter_window.  Testable without a GPU (tests/test_dist_gloo.py runs this
+ * plan over gloo).  GC_EINVAL on inconsistent arguments (rank 0 must start at row 0, the
+ * last rank must end at H_global, H_band > halo when world > 1).
+ */
+gc_status gc_band_exchange_plan(int H_band, int W, int H_global, int row0, int rank, int world,
+                                float sigma_s, int op, gc_band_xfer xfer[2], int seg_row0[3],
+                                int seg_rows[3]);
 
 /* NCCL communicator owned by the library.  gc_comm_unique_id fills 128 bytes on one
    rank; the caller broadcasts them (e.g. torch.distributed); every rank then calls
-   gc_comm_init.  GC_ENCCL on failure.  The CUDA device must be set by the caller. */
+   gc_comm_init.  GC_ENCCL on failure.  The CUDA device must be set by the caller.
+   `comm` arguments below are that handle (an ncclComm_t passed as void*). */
 gc_status gc_comm_unique_id(unsigned char id[128]);
 gc_status gc_comm_init(int rank, int world, const unsigned char id[128], void** comm_out);
 gc_status gc_comm_destroy(void* comm);
 
 /*
- * gc_bilateral_band — this rank's band of the GCF of the global image.  band / out:
- * device pointers to H_band*W fp32 (rows [row0, row0+H_band)).  Collective over comm:
- * exchanges the halo rows of f (not of the N+2 planes: they are pointwise in f, so
- * f is the smallest thing to send) with ranks r-1 and r+1 by grouped
- * ncclSend/ncclRecv on `stream`, then filters; symmetric extension only at global rows
- * 0 and H_global-1.  The result equals rows [row0, row0+H_band) of gc_filter on the
- * whole image.  Errors as gc_filter, plus GC_ENCCL.
+ * gc_comm_wait — host-blocking watchdog for the band exchange: waits until all work on
+ * `stream` has completed (GC_OK), polling ncclCommGetAsyncError every ~50 us.  An
+ * asynchronous NCCL error aborts the communicator (ncclCommAbort) and returns GC_ENCCL; no
+ * completion within timeout_ms (e.g. a peer failed before posting its half of the
+ * exchange) aborts it and returns GC_ETIMEOUT.  After an abort the communicator must be
+ * destroyed and re-created.  GC_ECUDA if the stream reports a CUDA error.
+ */
+gc_status gc_comm_wait(void* comm, void* stream, double timeout_ms);
+
+/*
+ * gc_bilateral_band — SURVEY §8(b)'s band entry point: this rank's band of the GCF of the
+ * global image, with (sigma_s, sigma_r, N) and the defaults of gc_params_init (L = 0,
+ * U = 255, eq. 19 coefficients, GC_OP_AUTO).  band / out: device pointers to H_band*W fp32
+ * (rows [row0, row0+H_band)).  comm: the ncclComm_t from gc_comm_init (as void*; §8(b)
+ * writes it as ncclComm_t).  Collective over comm: exchanges the halo rows of f (not of the
+ * N+2 planes: they are pointwise in f, so f is the smallest thing to send) with ranks r-1
+ * and r+1 by grouped ncclSend/ncclRecv on `stream` (the plan of gc_band_exchange_plan), then
+ * filters; symmetric extension only at global rows 0 and H_global-1.  The result equals
+ * rows [row0, row0+H_band) of gc_filter on the whole image.  Errors as gc_filter, plus
+ * GC_ENCCL.  Argument errors are returned before any NCCL call; an error after that
+ * (allocation, NCCL) leaves the peers' exchange incomplete: gc_comm_wait detects it.
  */
 gc_status gc_bilateral_band(const float* band, int H_band, int W, int H_global, int row0,
-                            const gc_params* p, float* out, void* comm, void* stream);
+                            float sigma_s, float sigma_r, int N, float* out, void* comm,
+                            void* stream);
+
+/* gc_filter_band — gc_bilateral_band with the full parameter struct (operator, caller
+   coefficients, guard counter, timing events recorded around the two filter passes). */
+gc_status gc_filter_band(const float* band, int H_band, int W, int H_global, int row0,
+                         const gc_params* p, float* out, void* comm, void* stream);
+
+/*
+ * gc_scratch_trim — release reserved stream-ordered scratch of libgc's private memory pool
+ * of the current device back to the driver, keeping at most keep_bytes reserved.  libgc
+ * never uses the device's default pool; by default its pool keeps freed scratch (the c5
+ * plane buffer is 14 GiB) for the next call.  GC_POOL_RELEASE_BYTES (environment, read once
+ * per device) bounds what it keeps.  Call after synchronising the streams libgc used.
+ */
+gc_status gc_scratch_trim(size_t keep_bytes);
 
 /*
  * gc_filter_window — single-GPU building block of the band path (and of the

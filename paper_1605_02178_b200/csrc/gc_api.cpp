@@ -46,7 +46,7 @@ std::vector<double> taps_of(float sigma_s, int R) {
 
 // Constants of the O(1) exact-window operator (gc_o1.cu, gc_operator.cpp).
 void o1_constants(float sigma_s, KParams& k) {
-  const O1Fit& f = o1_fit_cached(sigma_s);
+  const O1Fit f = o1_fit_cached(sigma_s);
   for (int q = 0; q < kO1K; q++) {
     const double w = f.omega[q];
     const double sh = std::sin(0.5 * w);
@@ -96,10 +96,8 @@ gc_status fill_constants(const gc_params* p, KParams& k, std::vector<float2>& ta
     if (!(mx > 0) || !std::isfinite(mx)) return GC_ERANGE;
     for (auto& v : cm) v /= mx;
   } else {
-    const double* cmu = nullptr;
-    gc_status st = coeffs_cached(p->N, p->sigma_r, L, U, nullptr, &cmu, nullptr);
+    gc_status st = coeffs_cached(p->N, p->sigma_r, L, U, nullptr, &cm, nullptr);
     if (st != GC_OK) return st;
-    std::copy(cmu, cmu + p->N + 1, cm.begin());
   }
   const int planes = ((p->N + 2) + 1) / 2 * 2;
   k.NP = planes / 2;
@@ -144,22 +142,43 @@ gc_status cuda_status(cudaError_t e) {
   return GC_ECUDA;
 }
 
-// Keep freed stream-ordered scratch in the device's default pool instead of returning it
-// to the driver at every synchronisation (the plane buffer is reallocated per call).
-void retain_pool() {
+}  // namespace
+
+// Stream-ordered scratch comes from a libgc-private memory pool per device, never from the
+// device's default pool (which PyTorch and other libraries share).  Freed blocks
+// stay reserved in the private pool up to its release threshold: unbounded by default, since
+// the c5 plane buffer is 14 GiB and re-mapping it on every call costs milliseconds.  The
+// environment variable GC_POOL_RELEASE_BYTES bounds it; gc_scratch_trim() hands reserved
+// memory back to the driver on demand.
+cudaMemPool_t scratch_pool() {
   static std::mutex mu;
-  static bool done[64] = {false};
+  static cudaMemPool_t pools[64] = {};
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
   std::lock_guard<std::mutex> lk(mu);
-  if (done[dev]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pl = nullptr;
+    if (cudaMemPoolCreate(&pl, &props) != cudaSuccess) return nullptr;
     uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    if (const char* env = std::getenv("GC_POOL_RELEASE_BYTES")) thr = std::strtoull(env, nullptr, 10);
+    cudaMemPoolSetAttribute(pl, cudaMemPoolAttrReleaseThreshold, &thr);
+    pools[dev] = pl;
   }
-  done[dev] = true;
+  return pools[dev];
 }
+
+cudaError_t scratch_alloc(void** ptr, size_t bytes, cudaStream_t s) {
+  cudaMemPool_t pl = scratch_pool();
+  if (!pl) return cudaErrorInitializationError;
+  return cudaMallocFromPoolAsync(ptr, bytes, pl, s);
+}
+
+namespace {
 
 // Per-device copy-in / copy-out streams and a second compute stream of gc_filter_host
 // (created once, never destroyed).
@@ -218,7 +237,6 @@ EventPool& event_pool() {
 
 // Run the pipeline for the window described by k (rows/segments already set).
 gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) {
-  retain_pool();
   int dev = 0;
   cudaGetDevice(&dev);
   k.num_sms = 148;
@@ -231,7 +249,7 @@ gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) 
   const size_t elem = k.fp64 ? sizeof(double2) : sizeof(float2);
   // (Deriche mode: a second plane-sized buffer after the counters for the causal partial sums)
   const size_t scratch_elems = op == GC_OP_DERICHE ? plane_elems * k.B : 0;
-  cudaError_t e = cudaMallocAsync((void**)&planes, plane_elems * k.B * elem + 256 + scratch_elems * elem, s);
+  cudaError_t e = scratch_alloc((void**)&planes, plane_elems * k.B * elem + 256 + scratch_elems * elem, s);
   if (e != cudaSuccess) return cuda_status(e);
   k.counters = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(planes) + plane_elems * k.B * elem);
   k.scratch = scratch_elems ? reinterpret_cast<float2*>(reinterpret_cast<char*>(k.counters) + 256) : nullptr;
@@ -245,7 +263,7 @@ gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) 
       src = td.data();
       bytes = td.size() * sizeof(double);
     }
-    e = cudaMallocAsync((void**)&taps_dev, bytes, s);
+    e = scratch_alloc((void**)&taps_dev, bytes, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(taps_dev, src, bytes, cudaMemcpyHostToDevice, s);
     // (pageable source: cudaMemcpyAsync returns once the bytes are staged, td may then go)
     if (e != cudaSuccess) {
@@ -283,11 +301,18 @@ const char* gc_status_string(gc_status s) {
     case GC_ECUDA: return "GC_ECUDA: CUDA error";
     case GC_ENOMEM: return "GC_ENOMEM: device allocation failed";
     case GC_ENCCL: return "GC_ENCCL: NCCL error";
+    case GC_ETIMEOUT: return "GC_ETIMEOUT: collective did not complete in time (communicator aborted)";
   }
   return "GC_?: unknown status";
 }
 
-const char* gc_version(void) { return "gc 0.1.0 sm_100a"; }
+const char* gc_version(void) { return "gc 0.2.0 sm_100a"; }
+
+gc_status gc_scratch_trim(size_t keep_bytes) {
+  cudaMemPool_t pl = scratch_pool();
+  if (!pl) return GC_ECUDA;
+  return cuda_status(cudaMemPoolTrimTo(pl, keep_bytes));
+}
 
 void gc_params_init(gc_params* p, int N, float sigma_s, float sigma_r) {
   if (!p) return;
@@ -437,7 +462,7 @@ gc_status gc_operator_taps(float sigma_s, int op, double* taps_out, int* W_out) 
     const std::vector<double> t = taps_of(sigma_s, R);
     std::copy(t.begin(), t.end(), taps_out);
   } else {
-    const O1Fit& f = o1_fit_cached(sigma_s);
+    const O1Fit f = o1_fit_cached(sigma_s);
     for (int m = -R; m <= R; m++) {
       double v = 0;
       for (int q = 0; q < kO1K; q++) v += f.alpha[q] * std::cos(f.omega[q] * m);
@@ -481,9 +506,9 @@ gc_status gc_filter_host(const float* imgs_host, int B, int H, int W, const gc_p
   const auto t_host0 = std::chrono::steady_clock::now();
   const size_t bytes = (size_t)B * H * W * sizeof(float);
   float *din = nullptr, *dout = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&din, bytes, s);
+  cudaError_t e = scratch_alloc((void**)&din, bytes, s);
   if (e != cudaSuccess) return cuda_status(e);
-  e = cudaMallocAsync((void**)&dout, bytes, s);
+  e = scratch_alloc((void**)&dout, bytes, s);
   if (e != cudaSuccess) { cudaFreeAsync(din, s); return cuda_status(e); }
   // Pipeline: the input is copied in K chunks on a copy-in stream, each chunk is filtered on
   // `s` as soon as the rows it reads have arrived, and copied back on a copy-out stream, so the

@@ -7,7 +7,9 @@
 // one node), then the band is filtered by gc_filter_window with three input segments
 // (top halo, own band, bottom halo).  Symmetric extension is applied only at the
 // global rows 0 and H-1, so the result equals the single-GPU filter of the whole image.
+#include <chrono>
 #include <cmath>
+#include <thread>
 #include <cstring>
 #include <vector>
 
@@ -15,13 +17,24 @@
 
 #include "gc_internal.h"
 
+namespace {
+
+// Halo rows a band needs per side: W_s = ceil(3 sigma_s) for eq. (7); the Deriche
+// operator's lead-in K = ceil(10 sigma_s) for GC_OP_DERICHE.
+int band_halo(float sigma_s, int op) {
+  return (int)std::ceil((op == GC_OP_DERICHE ? 10.0 : 3.0) * (double)sigma_s);
+}
+
+}  // namespace
+
 extern "C" {
 
-gc_status gc_band_plan(int H_global, int rank, int world, const int* band_rows, float sigma_s, int* row0,
+gc_status gc_band_plan(int H_global, int rank, int world, const int* band_rows, float sigma_s, int op, int* row0,
                        int* top0, int* top_rows, int* bot0, int* bot_rows) {
   if (!band_rows || world < 1 || rank < 0 || rank >= world || H_global < 1) return GC_EINVAL;
   if (!(std::isfinite(sigma_s) && sigma_s > 0)) return GC_EINVAL;
-  const int R = (int)std::ceil(3.0 * (double)sigma_s);
+  if (op < GC_OP_AUTO || op > GC_OP_DERICHE) return GC_EINVAL;
+  const int R = band_halo(sigma_s, op);
   long long sum = 0, r0 = 0;
   for (int k = 0; k < world; k++) {
     if (band_rows[k] < 1) return GC_EINVAL;
@@ -36,6 +49,38 @@ gc_status gc_band_plan(int H_global, int rank, int world, const int* band_rows, 
   if (top_rows) *top_rows = rank > 0 ? R : 0;
   if (bot0) *bot0 = (int)r0 + hb;
   if (bot_rows) *bot_rows = rank < world - 1 ? R : 0;
+  return GC_OK;
+}
+
+gc_status gc_band_exchange_plan(int H_band, int W, int H_global, int row0, int rank, int world, float sigma_s,
+                                int op, gc_band_xfer xfer[2], int seg_row0[3], int seg_rows[3]) {
+  if (!xfer || !seg_row0 || !seg_rows || H_band < 1 || W < 1 || world < 1 || rank < 0 || rank >= world)
+    return GC_EINVAL;
+  if (row0 < 0 || row0 + H_band > H_global) return GC_EINVAL;
+  if (!(std::isfinite(sigma_s) && sigma_s > 0)) return GC_EINVAL;
+  if (op < GC_OP_AUTO || op > GC_OP_DERICHE) return GC_EINVAL;
+  if ((rank == 0) != (row0 == 0) || (rank == world - 1) != (row0 + H_band == H_global)) return GC_EINVAL;
+  const int R = band_halo(sigma_s, op);
+  const bool has_top = rank > 0, has_bot = rank < world - 1;
+  if ((has_top || has_bot) && H_band <= R) return GC_EINVAL;
+  const size_t halo = (size_t)R * W;
+  // xfer[0]: with rank-1 — my first R rows go up, the R rows above me come down
+  xfer[0].peer = has_top ? rank - 1 : -1;
+  xfer[0].send_offset = 0;
+  xfer[0].count = has_top ? halo : 0;
+  xfer[0].recv_row0 = row0 - R;
+  // xfer[1]: with rank+1 — my last R rows go down, the R rows below me come up
+  xfer[1].peer = has_bot ? rank + 1 : -1;
+  xfer[1].send_offset = has_bot ? (size_t)(H_band - R) * W : 0;
+  xfer[1].count = has_bot ? halo : 0;
+  xfer[1].recv_row0 = row0 + H_band;
+  // the three input segments gc_filter_window reads: top halo, own band, bottom halo
+  seg_row0[0] = row0 - R;
+  seg_rows[0] = has_top ? R : 0;
+  seg_row0[1] = row0;
+  seg_rows[1] = H_band;
+  seg_row0[2] = row0 + H_band;
+  seg_rows[2] = has_bot ? R : 0;
   return GC_OK;
 }
 
@@ -63,47 +108,70 @@ gc_status gc_comm_destroy(void* comm) {
   return ncclCommDestroy(reinterpret_cast<ncclComm_t>(comm)) == ncclSuccess ? GC_OK : GC_ENCCL;
 }
 
-gc_status gc_bilateral_band(const float* band, int H_band, int W, int H_global, int row0, const gc_params* p,
-                            float* out, void* comm, void* stream) {
-  if (!band || !out || !comm || !p || H_band < 1 || W < 1 || row0 < 0 || row0 + H_band > H_global)
-    return GC_EINVAL;
-  if (!(std::isfinite(p->sigma_s) && p->sigma_s > 0)) return GC_EINVAL;
+gc_status gc_comm_wait(void* comm, void* stream, double timeout_ms) {
+  if (!comm || !(timeout_ms >= 0)) return GC_EINVAL;
+  ncclComm_t c = reinterpret_cast<ncclComm_t>(comm);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return GC_OK;
+    if (q != cudaErrorNotReady) return GC_ECUDA;
+    ncclResult_t async = ncclSuccess;
+    if (ncclCommGetAsyncError(c, &async) != ncclSuccess || (async != ncclSuccess && async != ncclInProgress)) {
+      ncclCommAbort(c);                      // releases the NCCL kernels blocked on the stream
+      return GC_ENCCL;
+    }
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > timeout_ms) {
+      ncclCommAbort(c);                      // a peer never posted its half of the exchange
+      return GC_ETIMEOUT;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
+gc_status gc_filter_band(const float* band, int H_band, int W, int H_global, int row0, const gc_params* p,
+                         float* out, void* comm, void* stream) {
+  if (!band || !out || !comm || !p) return GC_EINVAL;
   ncclComm_t c = reinterpret_cast<ncclComm_t>(comm);
   int rank = 0, world = 1;
   if (ncclCommUserRank(c, &rank) != ncclSuccess || ncclCommCount(c, &world) != ncclSuccess) return GC_ENCCL;
-  // halo rows: W_s for eq. (7); the Deriche operator's lead-in K = ceil(10 sigma_s) for GC_OP_DERICHE
-  const int R = (int)std::ceil((p->op == GC_OP_DERICHE ? 10.0 : 3.0) * (double)p->sigma_s);
-  const bool has_top = rank > 0, has_bot = rank < world - 1;
-  if ((has_top || has_bot) && H_band <= R) return GC_EINVAL;
+  gc_band_xfer x[2];
+  int seg_row0[3], seg_rows[3];
+  gc_status st = gc_band_exchange_plan(H_band, W, H_global, row0, rank, world, p->sigma_s, p->op, x, seg_row0,
+                                       seg_rows);
+  if (st != GC_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const size_t halo = (size_t)R * W;
-  float *top = nullptr, *bot = nullptr;
-  if (has_top && cudaMallocAsync((void**)&top, halo * 4, s) != cudaSuccess) return GC_ENOMEM;
-  if (has_bot && cudaMallocAsync((void**)&bot, halo * 4, s) != cudaSuccess) {
-    if (top) cudaFreeAsync(top, s);
-    return GC_ENOMEM;
+  float* recv[2] = {nullptr, nullptr};
+  for (int k = 0; k < 2; k++) {
+    if (x[k].peer < 0) continue;
+    if (gc::scratch_alloc((void**)&recv[k], x[k].count * 4, s) != cudaSuccess) {
+      if (recv[0]) cudaFreeAsync(recv[0], s);
+      return GC_ENOMEM;
+    }
   }
-  gc_status st = GC_OK;
   if (ncclGroupStart() != ncclSuccess) st = GC_ENCCL;
-  if (st == GC_OK && has_top) {
-    // my first R rows go up; the R rows above me come down from rank-1
-    if (ncclSend(band, halo, ncclFloat32, rank - 1, c, s) != ncclSuccess) st = GC_ENCCL;
-    if (ncclRecv(top, halo, ncclFloat32, rank - 1, c, s) != ncclSuccess) st = GC_ENCCL;
-  }
-  if (st == GC_OK && has_bot) {
-    if (ncclSend(band + (size_t)(H_band - R) * W, halo, ncclFloat32, rank + 1, c, s) != ncclSuccess) st = GC_ENCCL;
-    if (ncclRecv(bot, halo, ncclFloat32, rank + 1, c, s) != ncclSuccess) st = GC_ENCCL;
+  for (int k = 0; k < 2 && st == GC_OK; k++) {
+    if (x[k].peer < 0) continue;
+    if (ncclSend(band + x[k].send_offset, x[k].count, ncclFloat32, x[k].peer, c, s) != ncclSuccess) st = GC_ENCCL;
+    if (ncclRecv(recv[k], x[k].count, ncclFloat32, x[k].peer, c, s) != ncclSuccess) st = GC_ENCCL;
   }
   if (ncclGroupEnd() != ncclSuccess) st = GC_ENCCL;
   if (st == GC_OK) {
-    const float* seg[3] = {has_top ? top : band, band, has_bot ? bot : band};
-    const int seg_row0[3] = {row0 - R, row0, row0 + H_band};
-    const int seg_rows[3] = {has_top ? R : 0, H_band, has_bot ? R : 0};
+    const float* seg[3] = {recv[0] ? recv[0] : band, band, recv[1] ? recv[1] : band};
     st = gc_filter_window(seg, seg_row0, seg_rows, H_global, W, row0, H_band, p, out, stream);
   }
-  if (top) cudaFreeAsync(top, s);
-  if (bot) cudaFreeAsync(bot, s);
+  if (recv[0]) cudaFreeAsync(recv[0], s);
+  if (recv[1]) cudaFreeAsync(recv[1], s);
   return st;
+}
+
+gc_status gc_bilateral_band(const float* band, int H_band, int W, int H_global, int row0, float sigma_s,
+                            float sigma_r, int N, float* out, void* comm, void* stream) {
+  gc_params p;
+  gc_params_init(&p, N, sigma_s, sigma_r);
+  return gc_filter_band(band, H_band, W, H_global, row0, &p, out, comm, stream);
 }
 
 }  // extern "C"

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "gc_internal.h"
+#include "gc_lru.h"
 #include "mpfloat.h"
 
 using gcmp::MPF;
@@ -116,8 +117,7 @@ CoefResult compute(int N, double sigma_r, double L, double U) {
   return r;
 }
 
-std::mutex g_mu;
-std::map<std::tuple<int, uint64_t, uint64_t, uint64_t>, CoefResult> g_cache;
+gc::LruMemo<std::tuple<int, uint64_t, uint64_t, uint64_t>, CoefResult> g_cache;   // bounded
 
 uint64_t bits_of(double x) { uint64_t b; std::memcpy(&b, &x, 8); return b; }
 
@@ -125,8 +125,8 @@ uint64_t bits_of(double x) { uint64_t b; std::memcpy(&b, &x, 8); return b; }
 
 namespace gc {
 
-gc_status coeffs_cached(int N, double sigma_r, double L, double U, const double** c, const double** cmu,
-                        double* mu) {
+gc_status coeffs_cached(int N, double sigma_r, double L, double U, std::vector<double>* c,
+                        std::vector<double>* cmu, double* mu) {
   if (N < 0 || !(sigma_r > 0) || !(U > L) || !std::isfinite(sigma_r) || !std::isfinite(L) || !std::isfinite(U))
     return GC_EINVAL;
   if (N > GC_N_MAX) return GC_ERANGE;
@@ -134,12 +134,10 @@ gc_status coeffs_cached(int N, double sigma_r, double L, double U, const double*
   if (!(mu_d <= GC_MU_MAX)) return GC_ERANGE;
   if (!(mu_d > 1e-30)) return GC_ERANGE;
   auto key = std::make_tuple(N, bits_of(sigma_r), bits_of(L), bits_of(U));
-  std::lock_guard<std::mutex> lk(g_mu);
-  auto it = g_cache.find(key);
-  if (it == g_cache.end()) it = g_cache.emplace(key, compute(N, sigma_r, L, U)).first;
-  if (c) *c = it->second.c.data();
-  if (cmu) *cmu = it->second.cmu.data();
-  if (mu) *mu = it->second.mu;
+  const CoefResult r = g_cache.get(key, [&]() { return compute(N, sigma_r, L, U); });
+  if (c) *c = r.c;
+  if (cmu) *cmu = r.cmu;
+  if (mu) *mu = r.mu;
   return GC_OK;
 }
 
@@ -147,11 +145,11 @@ gc_status coeffs_cached(int N, double sigma_r, double L, double U, const double*
 
 extern "C" gc_status gc_coeffs(int N, double sigma_r, double L, double U, double* c_out, double* mu_out) {
   if (!c_out) return GC_EINVAL;
-  const double* c = nullptr;
+  std::vector<double> c;
   double mu = 0;
   gc_status st = gc::coeffs_cached(N, sigma_r, L, U, &c, nullptr, &mu);
   if (st != GC_OK) return st;
-  std::memcpy(c_out, c, sizeof(double) * (N + 1));
+  std::memcpy(c_out, c.data(), sizeof(double) * (N + 1));
   if (mu_out) *mu_out = mu;
   return GC_OK;
 }

@@ -5,6 +5,7 @@
 #include <atomic>
 #include <cstdint>
 #include <utility>
+#include <vector>
 
 #include "../../include/gc.h"
 
@@ -13,8 +14,12 @@
 namespace gc {
 
 // Host coefficient cache (gc_coeffs.cpp): c_n (eq. 19) and the normalised c_n mu^n.
-gc_status coeffs_cached(int N, double sigma_r, double L, double U, const double** c,
-                        const double** cmu, double* mu);
+// Copies out of a bounded LRU memo (gc_lru.h); c / cmu / mu may be null.
+gc_status coeffs_cached(int N, double sigma_r, double L, double U, std::vector<double>* c,
+                        std::vector<double>* cmu, double* mu);
+
+// Stream-ordered scratch from libgc's private per-device pool (gc_api.cpp); free with cudaFreeAsync.
+cudaError_t scratch_alloc(void** ptr, size_t bytes, cudaStream_t s);
 
 constexpr int kMaxPlanes = GC_N_MAX + 2 + 1;   // N+2 planes, rounded up to even
 constexpr int kMaxPairs = (kMaxPlanes + 1) / 2;
@@ -94,7 +99,7 @@ struct O1Fit {
   double omega[kO1K];
   double fit_err;
 };
-const O1Fit& o1_fit_cached(float sigma_s);
+O1Fit o1_fit_cached(float sigma_s);
 
 // O(1) column pass: G lanes per column share the NP plane pairs, npg = ceil(NP / G) <= 7 each
 // (G = 1 up to 7 pairs: one lane holds every pair of its column, no cross-lane reduction).

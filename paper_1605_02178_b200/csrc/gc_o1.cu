@@ -356,7 +356,9 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const __grid_constant_
                             (long long)(p.out_row0 - p.seg[0].row0) * p.Wd + xc;
   // step i (window centred on output-relative row i): entering row i+R+1, leaving row i-R
   auto issue = [&](int i, int st) {
-    const int ye_row = mirror(p.out_row0 + i + R + 1, p.H) - p.in_row0;
+    // (the entering row of the last step feeds the window after ye, which is never output: at
+    // the bottom of an interior window it lies one row past the plane buffer, so clamp it)
+    const int ye_row = min(mirror(p.out_row0 + i + R + 1, p.H) - p.in_row0, p.in_rows - 1);
     // (during the lead-in the leaving sample is masked to zero; read a valid row instead)
     const int yl_row = i >= ys ? mirror(p.out_row0 + i - R, p.H) - p.in_row0 : ye_row;
     if (TMA) {

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "gc_internal.h"
+#include "gc_lru.h"
 
 namespace gc {
 namespace {
@@ -97,13 +98,9 @@ O1Fit compute_fit(float sigma_s) {
 
 }  // namespace
 
-const O1Fit& o1_fit_cached(float sigma_s) {
-  static std::mutex mu;
-  static std::map<float, O1Fit> cache;
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find(sigma_s);
-  if (it == cache.end()) it = cache.emplace(sigma_s, compute_fit(sigma_s)).first;
-  return it->second;
+O1Fit o1_fit_cached(float sigma_s) {
+  static LruMemo<float, O1Fit> cache;       // bounded; computed outside the lock
+  return cache.get(sigma_s, [&]() { return compute_fit(sigma_s); });
 }
 
 }  // namespace gc

@@ -52,39 +52,51 @@ def rect_ramp(H: int, W: int, seed: int, n_rect: int = 16, noise: float = 10.0) 
     return np.ascontiguousarray(img.astype(np.float32))
 
 
+VORONOI_CHUNK = 256   # rows per noise chunk (part of the recipe: chunk k's noise has its own stream)
+
+
 def voronoi_texture(H: int, W: int, seed: int, n_seeds: int, noise: float,
                     amp: float = 20.0, lam: float = 16.0, theta: float = math.pi / 6,
-                    chunk_rows: int = 256) -> np.ndarray:
+                    rows: tuple | None = None) -> np.ndarray:
     """c2/c3/c5 construction (BASELINE.json configs[1], [2], [4]).
 
     Draw order: seed x ~ U[0, W) (n_seeds), seed y ~ U[0, H) (n_seeds), cell
-    value ~ U[0, 255] (n_seeds), then noise N(0, noise^2) row-chunk by row-chunk.
-    Each pixel (x, y) takes the value of the seed nearest (Euclidean) to its
-    centre (x+0.5, y+0.5); texture amp*sin(2*pi*(x cos(theta) + y sin(theta))/lam)
-    is added (amp=0 disables it), then noise, then clip to [0, 255].
+    value ~ U[0, 255] (n_seeds), all from default_rng(seed).  Each pixel (x, y) takes the
+    value of the seed nearest (Euclidean) to its centre (x+0.5, y+0.5); texture
+    amp*sin(2*pi*(x cos(theta) + y sin(theta))/lam) is added (amp=0 disables it), then
+    noise N(0, noise^2), then clip to [0, 255].  The noise of row chunk k (rows
+    [256k, 256k+256)) is drawn from its own stream default_rng([seed, 1, k]), so any row
+    range can be generated on its own (rows=(r0, r1): rows r0..r1-1 of the H x W image,
+    identical to the same rows of the whole image) — each rank of the row-band bench
+    generates only its band and halos.
     """
     from scipy.spatial import cKDTree
 
+    r0, r1 = (0, H) if rows is None else (max(0, int(rows[0])), min(H, int(rows[1])))
     rng = np.random.default_rng(seed)
     sx = rng.uniform(0.0, W, size=n_seeds)
     sy = rng.uniform(0.0, H, size=n_seeds)
     val = rng.uniform(0.0, 255.0, size=n_seeds)
     tree = cKDTree(np.stack([sx, sy], axis=1))
-    out = np.empty((H, W), dtype=np.float32)
+    out = np.empty((max(0, r1 - r0), W), dtype=np.float32)
     xs = np.arange(W, dtype=np.float64)
     ct, st = math.cos(theta), math.sin(theta)
-    for r0 in range(0, H, chunk_rows):
-        r1 = min(H, r0 + chunk_rows)
-        ys = np.arange(r0, r1, dtype=np.float64)
+    C = VORONOI_CHUNK
+    for k in range(r0 // C, (r1 + C - 1) // C):
+        c0, c1 = k * C, min(H, (k + 1) * C)
+        nrng = np.random.default_rng([seed, 1, k])
+        nz = nrng.normal(0.0, noise, size=(c1 - c0, W))
+        a, b = max(c0, r0), min(c1, r1)             # rows of this chunk that are wanted
+        ys = np.arange(a, b, dtype=np.float64)
         X, Y = np.meshgrid(xs, ys)
         pts = np.stack([(X + 0.5).ravel(), (Y + 0.5).ravel()], axis=1)
         _, idx = tree.query(pts, k=1, workers=-1)
-        blk = val[idx].reshape(r1 - r0, W)
+        blk = val[idx].reshape(b - a, W)
         if amp != 0.0:
             blk = blk + amp * np.sin(2.0 * math.pi * (X * ct + Y * st) / lam)
-        blk = blk + rng.normal(0.0, noise, size=(r1 - r0, W))
+        blk = blk + nz[a - c0:b - c0]
         np.clip(blk, 0.0, 255.0, out=blk)
-        out[r0:r1] = blk.astype(np.float32)
+        out[a - r0:b - r0] = blk.astype(np.float32)
     return out
 
 
@@ -136,12 +148,14 @@ CONFIGS = {
 }
 
 
-def config_image(cfg: Config | str, index: int = 0, H: int | None = None, W: int | None = None) -> np.ndarray:
+def config_image(cfg: Config | str, index: int = 0, H: int | None = None, W: int | None = None,
+                 rows: tuple | None = None) -> np.ndarray:
     """Image `index` of config `cfg` (batch configs use seed cfg.seed + index).
 
     H/W override the size (same construction, used for reduced-size parity
     cases); the Voronoi seed count is scaled with the area so the cell size
-    stays that of the full config.
+    stays that of the full config.  rows=(r0, r1) returns only those rows of the
+    image (Voronoi constructions generate just them; the others slice).
     """
     if isinstance(cfg, str):
         cfg = CONFIGS[cfg]
@@ -150,9 +164,10 @@ def config_image(cfg: Config | str, index: int = 0, H: int | None = None, W: int
     seed = cfg.seed + index
     g = dict(cfg.gen)
     if cfg.kind == "rect":
-        return rect_ramp(H, W, seed, **g)
+        img = rect_ramp(H, W, seed, **g)
+        return img if rows is None else np.ascontiguousarray(img[max(0, rows[0]):rows[1]])
     if cfg.kind == "voronoi":
         if (H, W) != (cfg.H, cfg.W):
             g["n_seeds"] = max(1, int(round(g["n_seeds"] * H * W / (cfg.H * cfg.W))))
-        return voronoi_texture(H, W, seed, **g)
+        return voronoi_texture(H, W, seed, rows=rows, **g)
     raise ValueError(cfg.kind)

@@ -3,6 +3,7 @@ its host-only entry points (gc_coeffs, gc_band_plan) agree with the oracle / the
 paper, and argument validation returns the documented status codes before any CUDA
 work is enqueued.  No kernel is launched here."""
 import ctypes
+import math
 import os
 import re
 
@@ -113,8 +114,9 @@ def test_device_entry_points_validate_before_cuda(gc):
 
 def test_status_strings(gc):
     lib = gc.lib()
-    for s in range(6):
+    for s in range(7):
         assert lib.gc_status_string(s).startswith(b"GC_")
+    assert lib.gc_status_string(6).startswith(b"GC_ETIMEOUT")
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
@@ -139,6 +141,48 @@ def test_band_plan_errors(gc):
         gc.band_plan(100, 0, 2, [92, 8], 3.0)             # band <= W_s = 9
     with pytest.raises(gc.GCError):
         gc.band_plan(100, 2, 2, [50, 50], 3.0)            # rank out of range
+    gc.band_plan(100, 0, 2, [50, 50], 3.0)                # halo 9 < 50 rows: fine for eq. (7) ...
+    with pytest.raises(gc.GCError):
+        gc.band_plan(100, 0, 2, [50, 50], 5.0, op=gc.OP_DERICHE)   # ... Deriche needs K = 50 rows: rejected
+    with pytest.raises(gc.GCError):
+        gc.band_plan(100, 0, 2, [50, 50], 3.0, op=7)      # unknown operator
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("op", [0, 3])
+def test_band_exchange_plan(gc, world, op):
+    """gc_band_exchange_plan (what gc_filter_band sends, receives and filters): every halo row a
+    rank receives is exactly the rows its neighbour sends (offsets into the neighbour's band),
+    and the three segments cover [row0 - halo, row0 + H_band + halo) clipped to the image."""
+    H, W, sigma_s = 1000, 37, 4.0
+    halo = math.ceil((10 if op == 3 else 3) * sigma_s)
+    rows = [H // world + (1 if k < H % world else 0) for k in range(world)]
+    r0 = [sum(rows[:k]) for k in range(world)]
+    plans = [gc.band_exchange_plan(rows[k], W, H, r0[k], k, world, sigma_s, op) for k in range(world)]
+    for k, (xf, segs) in enumerate(plans):
+        up, down = xf
+        assert (up["peer"], down["peer"]) == (k - 1 if k > 0 else -1, k + 1 if k < world - 1 else -1)
+        assert segs[1] == (r0[k], rows[k])
+        assert segs[0] == (r0[k] - halo, halo if k > 0 else 0)
+        assert segs[2] == (r0[k] + rows[k], halo if k < world - 1 else 0)
+        for x, seg in ((up, segs[0]), (down, segs[2])):
+            if x["peer"] < 0:
+                assert x["count"] == 0
+                continue
+            assert x["count"] == halo * W and x["recv_row0"] == seg[0]
+            # what the peer sends to me starts at global row recv_row0
+            px = plans[x["peer"]][0][0 if x["peer"] == k + 1 else 1]
+            assert px["peer"] == k and px["count"] == x["count"]
+            assert r0[x["peer"]] + px["send_offset"] // W == x["recv_row0"] and px["send_offset"] % W == 0
+
+
+def test_band_exchange_plan_errors(gc):
+    with pytest.raises(gc.GCError):
+        gc.band_exchange_plan(50, 8, 100, 10, 0, 2, 3.0)     # rank 0 must start at row 0
+    with pytest.raises(gc.GCError):
+        gc.band_exchange_plan(40, 8, 100, 50, 1, 2, 3.0)     # last rank must end at H
+    with pytest.raises(gc.GCError):
+        gc.band_exchange_plan(8, 8, 16, 8, 1, 2, 3.0)        # band of 8 rows <= halo 9
 
 
 @pytest.mark.parametrize("sigma_s", [0.3, 1.0, 2.0, 3.0, 4.0, 5.0, 7.5, 10.0, 16.0, 20.0, 40.0, 100.0, 400.0])

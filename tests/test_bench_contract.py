@@ -14,9 +14,16 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 
 
+def test_default_workload_is_c5():
+    """The driver's default bench line runs the largest single-GPU configuration (c5, row bands at
+    N > 1) with K=20 / W=5."""
+    a = bench._args([])
+    assert a.workload == "c5" and a.gpus == 1 and a.steps >= 1 and a.warmup >= 3 and a.impl == "ours"
+
+
 def test_reference_arm_json_line():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
-                        "--warmup", "0"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+                        "--warmup", "0", "--workload", "c2"], capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0, r.stderr
     lines = [l for l in r.stdout.splitlines() if l.strip()]
     assert len(lines) == 1
@@ -25,7 +32,8 @@ def test_reference_arm_json_line():
     assert d["metric"] == bench.METRIC and d["higher_is_better"] is True
     assert d["config"]["workload"].startswith("c2") and d["config"]["N"] == 8
     cb = d["cpu_baseline"]
-    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+    assert cb["kind"] == "oracle" and cb["cores"] == len(os.sched_getaffinity(0)) and cb["value"] == d["value"]
+    assert cb["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
 
 
@@ -45,3 +53,57 @@ def test_deriche_bytes(N, NP):
     b = bench.dr_bytes(N, 1)
     assert (N + 3) // 2 == NP
     assert b == {"k_row": 8 + 24 * NP, "k_col": 8 + 32 * NP}
+
+
+def test_algorithmic_instruction_count():
+    """2(N+2)17 + 5N + 14 instructions per pixel (c2: 394, c5: 550); the column
+    pass's share (N+2)17 + 4(N+1) + 6 (c2: 212)."""
+    assert bench.alg_instr(8)["total"] == 394 and bench.alg_instr(12)["total"] == 550
+    assert bench.alg_instr(8)["k_col"] == 212
+    a = bench.alg_instr(12)
+    assert a["k_row"] + a["k_col"] == a["total"]
+    assert abs(bench.FP32_PEAK_TINSTR - 37.22) < 0.01
+
+
+def test_roofline_fields():
+    r = bench.roofline(12, 48, 2, 16384 * 16384, row_ms=5.0, col_ms=6.0, step_ms=11.0)
+    assert r["kernel"] == "k_col" and r["bound"] == "alu"
+    assert abs(r["achieved"] - bench.alg_instr(12)["k_col"] * 16384 ** 2 / 6e-3 / 1e12) < 1e-9
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-12
+    assert 0 < r["step_frac"] < r["frac"] * 2 and "derived" in r["peak_source"]
+
+
+@pytest.mark.parametrize("ws", [1, 2, 8])
+def test_check_rows_cover_every_seam(ws):
+    """The untimed oracle check includes, for every band seam b, rows b-W, b-1, b and b+W-1."""
+    from synth import CONFIGS
+    cfg = CONFIGS["c5"]
+    rows = [cfg.H // ws] * ws
+    chk = bench.check_rows(cfg, 16.0, ws, rows)
+    b = 0
+    for hb in rows[:-1]:
+        b += hb
+        assert {b - 48, b - 1, b, b + 47} <= set(chk)
+    assert 0 in chk and cfg.H - 1 in chk
+
+
+def test_oracle_check_crop_is_exact():
+    """oracle_check's crops reproduce the whole-image oracle (edge and interior rows)."""
+    import numpy as np
+    import dataclasses
+
+    import oracle
+    import synth
+    from synth import CONFIGS, config_image
+    cfg = dataclasses.replace(CONFIGS["c2"], H=96, W=80)
+    img = config_image("c2", H=96, W=80)
+    cfg = dataclasses.replace(cfg, gen=dict(cfg.gen, n_seeds=max(1, round(200 * 96 * 80 / 1024 ** 2))))
+    rows = [0, 3, 40, 95]
+    ref, _ = oracle.gc_filter_rows(img, rows, 5.0, 70.0, 8)
+    real = synth.config_image
+    try:
+        synth.config_image = lambda c, index=0, rows=None: real("c2", index, H=96, W=80, rows=rows)
+        chk = bench.oracle_check(cfg, 5.0, 70.0, rows, ref.astype(np.float32), cols=32)
+    finally:
+        synth.config_image = real
+    assert chk["max_abs"] < 1e-4 and chk["pass"]

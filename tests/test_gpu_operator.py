@@ -149,10 +149,16 @@ def test_band_path_single_rank_nccl(gc):
     img = config_image("c5", H=300, W=260)
     t = torch.from_numpy(img).cuda()
     for s in [3.0, 16.0]:
-        band = gc.bilateral_band(t, 300, 0, s, 55.0, 12, comm)
+        band = gc.bilateral_band(t, 300, 0, s, 55.0, 12, comm)                 # SURVEY 8(b) signature
+        full = gc.bilateral_band(t, 300, 0, s, 55.0, 12, comm, op=gc.OP_O1)    # gc_filter_band
         whole = gc.filter(t, s, 55.0, 12)
+        comm.wait(timeout_ms=60000)                                             # gc_comm_wait: idle -> OK
         torch.cuda.synchronize()
         assert torch.equal(band, whole)
+        if s > 8:
+            assert torch.equal(full, whole)                                     # AUTO resolves to O1 here
+    with pytest.raises(ValueError):
+        gc.bilateral_band(t, 300, 0, 3.0, 55.0, 12, comm, out=torch.empty((299, 260), device="cuda"))
     comm.close()
     dist.destroy_process_group()
 
@@ -192,3 +198,26 @@ def test_maximum_degree_and_radius(gc, op):
     ref, _ = oracle.gc_filter(img, s, 100.0, 5)
     out = gc.filter(t, s, 100.0, 5, op=op).cpu().numpy().astype(np.float64)
     assert np.max(np.abs(out - ref)) <= MAX_ABS
+
+
+def test_out_buffer_checks_and_scratch_trim(gc):
+    """caller-supplied `out` buffers are checked (shape, dtype, contiguity, device)
+    before libgc writes through them; the private scratch pool can be trimmed."""
+    import torch
+    img = torch.from_numpy(config_image("c2", H=64, W=80)).cuda()
+    with pytest.raises(ValueError):
+        gc.filter(img, 3.0, 70.0, 8, out=torch.empty((64, 79), device="cuda"))
+    with pytest.raises(TypeError):
+        gc.filter(img, 3.0, 70.0, 8, out=torch.empty((64, 80), device="cuda", dtype=torch.float16))
+    with pytest.raises(TypeError):
+        gc.filter(img, 3.0, 70.0, 8, out=torch.empty((80, 64), device="cuda").t())
+    with pytest.raises(TypeError):
+        gc.filter_host(img.cpu().numpy(), 3.0, 70.0, 8, out=np.empty((64, 40), np.float32))
+    with pytest.raises(TypeError):
+        gc.filter_host(img.cpu().numpy(), 3.0, 70.0, 8, out=np.empty((64, 80), np.float64))
+    a = gc.filter(img, 3.0, 70.0, 8)
+    torch.cuda.synchronize()
+    gc.scratch_trim(0)
+    b = gc.filter(img, 3.0, 70.0, 8)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)

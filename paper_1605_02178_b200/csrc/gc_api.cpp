@@ -50,10 +50,11 @@ void o1_constants(float sigma_s, KParams& k) {
   for (int q = 0; q < kO1K; q++) {
     const double w = f.omega[q];
     const double sh = std::sin(0.5 * w);
+    // alpha_q folded into the recursion inputs (gc_o1.cu: the states are alpha_q S_q)
     k.o1_alpha[q] = (float)f.alpha[q];
     k.o1_nk[q] = (float)(-4.0 * sh * sh);
-    k.o1_a[q] = (float)std::cos(w * f.R);
-    k.o1_nb[q] = (float)(-std::cos(w * (f.R + 1)));
+    k.o1_a[q] = (float)(f.alpha[q] * std::cos(w * f.R));
+    k.o1_nb[q] = (float)(-f.alpha[q] * std::cos(w * (f.R + 1)));
   }
 }
 

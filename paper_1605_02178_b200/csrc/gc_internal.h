@@ -68,11 +68,12 @@ struct KParams {
   // O(1) exact-window operator (gc_o1.cu): k_m ~ sum_q alpha_q cos(w_q m) on |m| <= W
   float o1_alpha[kO1K];            // alpha_q (q = 0: box term)
   float o1_nk[kO1K];               // -4 sin^2(w_q / 2)   (Reinsch form of the resonator)
-  float o1_a[kO1K];                // cos(w_q W)
-  float o1_nb[kO1K];               // -cos(w_q (W + 1))
+  float o1_a[kO1K];                // alpha_q cos(w_q W)        (alpha folded into the states)
+  float o1_nb[kO1K];               // -alpha_q cos(w_q (W + 1))
   int o1_seg_x, o1_nseg_x;         // row pass: x-segment length (multiple of 32) and count
   int o1_seg_y, o1_nseg_y;         // column pass: y-segment length and count
   int o1_groups;                   // row pass: plane-pair groups (<= 4 pairs each)
+  int o1_stages, o1_stages_l;      // pair-parallel column pass: entering / leaving TMA ring stages
   int raw;                         // 1: eq. (7) of f itself (gc_gaussian): pair 0 = (f, 0), out = Fbar_0
   // Deriche-class recursive operator (gc_deriche.cu; GC_OP_DERICHE): two 2nd-order sections per
   // direction, 1/Z folded into b0, b1, c1, c2

@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include <cuda.h>
@@ -45,31 +46,55 @@ namespace gc {
 constexpr int kO1Warps = 4;     // warps per CTA (independent tasks)
 constexpr int kO1CH = 16;       // positions per staged chunk
 constexpr int kO1TS = 17;       // staged tile row stride (float2): 2 wavefronts per warp access
-constexpr int kO1OC = 8;        // output positions per store chunk (= main-loop unroll)
+constexpr int kO1OC = 4;        // output positions per store chunk (= main-loop unroll)
 constexpr int kO1RowNPG = 4;    // plane pairs per row-pass warp (max)
-constexpr int kO1OS = 36;       // out tile position stride (float2): 2 wavefronts per access
+constexpr int kO1OS = 36;       // out tile position stride (float2): conflict-free 64-bit reads
+constexpr int kO1RS = 20;       // raw f row stride (floats): 16-byte cp.async rows, LDS.128 conflict-free
 
 struct RowO1Smem {
   float2 fin[32 * kO1TS];                  // entering stream  [row][pos] = (e a'^{2p0}, a')
   float2 fout[32 * kO1TS];                 // leaving stream   [row][pos]
   float2 o[kO1RowNPG][kO1OC][kO1OS];       // filtered pairs   [pair][pos][row]
+  float raw[2][32 * kO1RS];                // f of the NEXT chunk of each stream (cp.async prefetch)
 };
+
+// Prefetch f of this lane's row at the 16 positions [pc, pc+16) (whole-sample mirroring in x)
+// into raw (one cp.async group per call): the stage one chunk later finds it in shared memory
+// instead of stalling on DRAM (ncu r01: long_scoreboard was the top stall of k_row_o1).
+__device__ __forceinline__ void o1_prefetch_row(const KParams& p, float* raw, const float* rowp, int pc, int lane,
+                                               bool vec) {
+  float* d = raw + lane * kO1RS;
+  const unsigned s = (unsigned)__cvta_generic_to_shared(d);
+  if (vec && pc >= 0 && pc + kO1CH <= p.Wd) {
+#pragma unroll
+    for (int k = 0; k < kO1CH / 4; k++)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s + 16 * k), "l"(rowp + pc + 4 * k) : "memory");
+  } else {
+#pragma unroll 1
+    for (int k = 0; k < kO1CH; k++)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s + 4 * k), "l"(rowp + mirror(pc + k, p.Wd))
+                   : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
 
 // Stage this lane's row at the 16 positions of the aligned chunk [pc, pc+16) (whole-sample
 // mirroring in x) as v = (F'_{2p0}, a') = (e a'^{2p0}, a') of eq. (6), or (f, 0) for
 // gc_gaussian; then F'_{2p0+1} = v.x v.y and the pair step is a'^2 = v.y^2.
-__device__ __forceinline__ void o1_stage_row(const KParams& p, float2* t, const float* rowp, int pc, int lane,
-                                            bool vec, int p0) {
+// (f comes from the prefetch buffer `raw`, whose cp.async group the caller has waited for; the
+// next chunk of the same stream is prefetched into it afterwards)
+template <int WAIT>
+__device__ __forceinline__ void o1_stage_row(const KParams& p, float2* t, float* raw, const float* rowp, int pc,
+                                            int lane, bool vec, int p0) {
+  asm volatile("cp.async.wait_group %0;" ::"n"(WAIT) : "memory");
   float v[kO1CH];
-  if (vec && pc >= 0 && pc + kO1CH <= p.Wd) {
+  {
+    const float4* r4 = reinterpret_cast<const float4*>(raw + lane * kO1RS);
 #pragma unroll
     for (int k = 0; k < kO1CH / 4; k++) {
-      const float4 u = __ldg(reinterpret_cast<const float4*>(rowp + pc) + k);
+      const float4 u = r4[k];
       v[4 * k] = u.x; v[4 * k + 1] = u.y; v[4 * k + 2] = u.z; v[4 * k + 3] = u.w;
     }
-  } else {
-#pragma unroll
-    for (int k = 0; k < kO1CH; k++) v[k] = __ldg(rowp + mirror(pc + k, p.Wd));
   }
   float2* d = t + lane * kO1TS;
   __syncwarp();
@@ -104,14 +129,20 @@ __device__ __forceinline__ void o1_stage_row(const KParams& p, float2* t, const 
       d[k] = make_float2(e * pw, a);
     }
   }
+  // this stream's next chunk, issued after v has been consumed (the copy overwrites raw)
+  o1_prefetch_row(p, raw, rowp, pc + kO1CH, lane, vec);
   __syncwarp();
 }
 
 // One step of the exact-window recursion for one plane pair (Reinsch form).
 //   A = x(i+W+1) + x(i-W-1), B = x(i+W) + x(i-W), box: S0 += x(i+W+1) - x(i-W)
+// The fit weights alpha_q are folded into the state (S'_q = alpha_q S_q, a linear recursion with
+// inputs scaled by alpha_q: o1_a / o1_nb carry alpha_q, the box input alpha_0), so the filtered
+// value is the plain sum of the states (a 3-deep add tree instead of a 6-deep FMA chain).
+// The state-only FMA comes first: the input samples A, B (shared-memory loads) arrive last.
 __device__ __forceinline__ void o1_update(const KParams& p, float2& S0, float2* S, float2* D, float2 A, float2 B,
                                           float2 xin, float2 xout) {
-  S0 = f2add(S0, f2sub(xin, xout));
+  S0 = f2fma(f2s(p.o1_alpha[0]), f2sub(xin, xout), S0);
 #pragma unroll
   for (int t = 0; t < kO1K - 1; t++) {
     float2 d = f2fma(f2s(p.o1_nk[t + 1]), S[t], D[t]);
@@ -123,10 +154,8 @@ __device__ __forceinline__ void o1_update(const KParams& p, float2& S0, float2* 
 }
 
 __device__ __forceinline__ float2 o1_output(const KParams& p, float2 S0, const float2* S) {
-  float2 y = f2mul(f2s(p.o1_alpha[0]), S0);
-#pragma unroll
-  for (int t = 0; t < kO1K - 1; t++) y = f2fma(f2s(p.o1_alpha[t + 1]), S[t], y);
-  return y;
+  static_assert(kO1K == 6, "o1_output's add tree assumes the box + 5 resonators");
+  return f2add(f2add(f2add(S0, S[0]), f2add(S[1], S[2])), f2add(S[3], S[4]));
 }
 
 template <int NPG>
@@ -140,8 +169,10 @@ __device__ __forceinline__ void row_o1_step(const KParams& p, RowO1Smem& sm, Row
                                             const float* rowp, bool vec, int p0, int lane) {
   const int R = p.R;
   const int pe_pos = x + R + 1, pl_pos = x - R;
-  if ((pe_pos & (kO1CH - 1)) == 0) o1_stage_row(p, sm.fin, rowp, pe_pos, lane, vec, p0);
-  if ((pl_pos & (kO1CH - 1)) == 0) o1_stage_row(p, sm.fout, rowp, pl_pos, lane, vec, p0);
+  // the two streams stage on different steps ((2W+1) is odd), so the newest cp.async group is
+  // always the other stream's prefetch: wait_group 1 finds this stream's chunk complete
+  if ((pe_pos & (kO1CH - 1)) == 0) o1_stage_row<1>(p, sm.fin, sm.raw[0], rowp, pe_pos, lane, vec, p0);
+  if ((pl_pos & (kO1CH - 1)) == 0) o1_stage_row<1>(p, sm.fout, sm.raw[1], rowp, pl_pos, lane, vec, p0);
   const float2 ve = sm.fin[lane * kO1TS + (pe_pos & (kO1CH - 1))];
   const float2 vl = sm.fout[lane * kO1TS + (pl_pos & (kO1CH - 1))];
   float2 pe = make_float2(ve.x, ve.x * ve.y), pl = make_float2(vl.x, vl.x * vl.y);
@@ -174,10 +205,13 @@ __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int
   const bool vec = ((p.Wd & 3) == 0) && ((reinterpret_cast<uintptr_t>(rowp) & 15) == 0);
 
   // ---- lead-in: windows xs-2W-1 .. xs-1 (leaving samples are still zero)
+  o1_prefetch_row(p, sm.raw[0], rowp, P0 & ~(kO1CH - 1), lane, vec);
+  o1_prefetch_row(p, sm.raw[1], rowp, (xs - R) & ~(kO1CH - 1), lane, vec);
 #pragma unroll 1
   for (int s = 0; s < lead; s++) {
     const int pos = P0 + s;
-    if (s == 0 || (pos & (kO1CH - 1)) == 0) o1_stage_row(p, sm.fin, rowp, pos & ~(kO1CH - 1), lane, vec, p0);
+    if (s == 0 || (pos & (kO1CH - 1)) == 0)      // (only this stream stages here: wait for all groups)
+      o1_stage_row<0>(p, sm.fin, sm.raw[0], rowp, pos & ~(kO1CH - 1), lane, vec, p0);
     const float2 ve = sm.fin[lane * kO1TS + (pos & (kO1CH - 1))];
     float2 pe = make_float2(ve.x, ve.x * ve.y);
     const float a2e = ve.y * ve.y;
@@ -188,13 +222,16 @@ __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int
       pe = f2mul(pe, f2s(a2e));
     }
   }
-  // ---- outputs x = xs .. xe-1, in chunks of 8 positions (xs is a multiple of 32)
-  o1_stage_row(p, sm.fout, rowp, (xs - R) & ~(kO1CH - 1), lane, vec, p0);
+  // ---- outputs x = xs .. xe-1, in chunks of kO1OC positions (xs is a multiple of 32).  The
+  // leaving stream's first chunk: staged here unless x = xs itself starts a chunk (then the first
+  // step stages it; staging it twice would read the prefetch of the chunk after it)
+  if ((xs - R) & (kO1CH - 1)) o1_stage_row<0>(p, sm.fout, sm.raw[1], rowp, (xs - R) & ~(kO1CH - 1), lane, vec, p0);
   // O(1) plane layout [B][rows][NP][Wd]: the NP pairs of one image row are adjacent rows of
   // a 2-D [B*rows*NP][Wd] tensor, so the column pass fetches a row's pairs with one TMA box
   const long long rstride = (long long)p.NP * p.Wd;         // float2 between image rows
-  const int orow = lane >> 3, ocol = lane & 7;
-  const int rows_left = p.in_rows - (r0 + orow);            // rows r0+orow+4j valid for 4j < rows_left
+  constexpr int ORS = 32 / kO1OC;                           // rows per store instruction
+  const int orow = lane / kO1OC, ocol = lane % kO1OC;
+  const int rows_left = p.in_rows - (r0 + orow);            // rows r0+orow+ORS j valid for ORS j < rows_left
   float2* const obase = p.planes + b * p.planes_img_stride + (long long)(r0 + orow) * rstride +
                         (long long)p0 * p.Wd + ocol;
 #pragma unroll 1
@@ -202,20 +239,21 @@ __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int
     const int nb = min(kO1OC, xe - x);
 #pragma unroll 1
     for (int j = 0; j < nb; j++) row_o1_step<NPG>(p, sm, st, x + j, j, rowp, vec, p0, lane);
-    // store the chunk: per pair, 8 positions x 32 rows (4 rows x 64 bytes per instruction)
+    // store the chunk: per pair, kO1OC positions x 32 rows (ORS rows x 8 kO1OC bytes per instruction)
     __syncwarp();
     if (ocol < nb) {
       float2* o = obase + x;
 #pragma unroll
       for (int q = 0; q < NPG; q++) {
 #pragma unroll
-        for (int j = 0; j < 8; j++)
-          if (4 * j < rows_left) o[(long long)(4 * j) * rstride] = sm.o[q][ocol][4 * j + orow];
+        for (int j = 0; j < 32 / ORS; j++)
+          if (ORS * j < rows_left) o[(long long)(ORS * j) * rstride] = sm.o[q][ocol][ORS * j + orow];
         o += p.Wd;
       }
     }
     __syncwarp();
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");      // no copy may land after the task
 }
 
 __global__ void __launch_bounds__(32 * kO1Warps, 3) k_row_o1(const KParams p) {
@@ -227,10 +265,13 @@ __global__ void __launch_bounds__(32 * kO1Warps, 3) k_row_o1(const KParams p) {
   const int ntask = nrb * p.o1_nseg_x * p.o1_groups * p.B;
   const int task = blockIdx.x * kO1Warps + warp;
   if (task >= ntask) return;
-  const int g = task % p.o1_groups;
-  const int sx = (task / p.o1_groups) % p.o1_nseg_x;
-  const int rb = (task / (p.o1_groups * p.o1_nseg_x)) % nrb;
-  const int b = task / (p.o1_groups * p.o1_nseg_x * nrb);
+  // plane-pair group: rotated with the CTA index so that every SM sub-partition (warp % 4) gets
+  // a mix of the large and small groups (NP = 7: 4 + 3 pairs) instead of always the same one
+  const int rest = task / p.o1_groups;
+  const int g = (task % p.o1_groups + rest * p.o1_groups / kO1Warps) % p.o1_groups;
+  const int sx = rest % p.o1_nseg_x;
+  const int rb = (rest / p.o1_nseg_x) % nrb;
+  const int b = rest / (p.o1_nseg_x * nrb);
   const int xs = sx * p.o1_seg_x, xe = min(xs + p.o1_seg_x, p.Wd);
   const int p0 = g * kO1RowNPG;
   const int npl = min(kO1RowNPG, p.NP - p0);
@@ -468,12 +509,336 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const __grid_constant_
   count_guarded(p.fallback, 0xffffffffu, nguard);
 }
 
+// ------------------------------------------------------------------ pair-parallel column pass
+//
+// k_col_o1p<NP> (NP <= 8 plane pairs, even width): CTA = one 32-column strip x one y-segment;
+// warp q < NP runs the vertical recursion of plane pair q for the 32 columns (lane = column),
+// warp NP is the TMA producer.  Each step's entering row i+W+1 and leaving row i-W arrive as
+// two [NP pairs x 32 columns] TMA boxes into a kPD-stage ring (mbarrier full/empty per stage);
+// the consumers write their filtered pair of every output row into a [NP rows x NP pairs x 32]
+// shared tile and, every NP rows, each warp folds one row's NP pairs into P', Q' (eqs. 8-9)
+// and eq. (10).  Against k_col_o1 (one lane holds all NP pairs of its column): 1/NP of the
+// recursion state per thread (~60 instead of 254 registers), NP x the warps per column strip,
+// and — the point — a CTA's window of leaving rows is NP x 32 x (2W+1) x 8 B (174 KB at c5)
+// with only kO1PCtas CTAs per SM, so the whole GPU's in-flight windows (~51 MB at 2 CTAs/SM)
+// stay in L2 and the leaving rows are not re-read from HBM (k_col_o1 at c5: ~1200 resident
+// warps x 174 KB = 206 MB, 123 B/px of DRAM traffic instead of 64; profiles/r01_ncu_full_o1_c5.txt).
+
+constexpr int kPDMax = 48;       // ring stages per direction (at most)
+constexpr int kRPS = 4;          // image rows per ring stage: one [4 NP x 32] TMA box per direction in the
+                                 // interior (per-row boxes where the rows are mirrored or clamped)
+
+// Shared memory: this head, then the entering ring (nE stages) and the leaving ring (nL stages),
+// each stage kRPS rows x [NP pairs x 32 columns] float2.  Entering rows come from HBM (first
+// touch) and get the deep ring; leaving rows are the entering rows of 2W+1 steps earlier, kept in
+// L2 by the evict_last hint, and get a short ring.
+template <int NP>
+struct alignas(1024) ColPSmem {
+  unsigned long long full_e[kPDMax], empty_e[kPDMax], full_l[kPDMax], empty_l[kPDMax];
+  unsigned long long tile_full[2], tile_free[2];   // per tile buffer: all NP warps wrote / folded it
+  float2 tile[2][kRPS][NP][32];  // [buffer][row in block][pair][column]
+};
+template <int NP>
+__host__ __device__ constexpr size_t colp_head() { return (sizeof(ColPSmem<NP>) + 1023) / 1024 * 1024; }
+template <int NP>
+__host__ __device__ constexpr size_t colp_stage() { return (size_t)kRPS * NP * 32u * sizeof(float2); }
+
+__device__ __forceinline__ void o1_mbar_init_n(unsigned long long* bar, unsigned n) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s), "r"(n));
+}
+__device__ __forceinline__ void o1_mbar_arrive(unsigned long long* bar) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_test(unsigned bar, unsigned phase) {
+  unsigned ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ float2 lds64(unsigned a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts64(unsigned a, float2 v) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void tma_2d_u32(unsigned dst, const CUtensorMap* map, int c0, int c1, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+// 2-D TMA load with an L2 cache-policy hint (createpolicy descriptor)
+__device__ __forceinline__ void tma_2d_hint(unsigned dst, const CUtensorMap* map, int c0, int c1, unsigned bar,
+                                            unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "l"(pol)
+      : "memory");
+}
+
+template <int NP>
+__global__ void __launch_bounds__(32 * (NP + 1), 3)
+    k_col_o1p(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap4, const KParams p) {
+  extern __shared__ __align__(1024) float4 smem_o1p[];
+  ColPSmem<NP>& sm = *reinterpret_cast<ColPSmem<NP>*>(smem_o1p);
+  constexpr unsigned BOX = NP * 32u * 8u;           // one image row: [NP pairs x 32 columns]
+  constexpr unsigned SB = kRPS * BOX;               // one stage (kRPS rows)
+  const int nE = p.o1_stages, nL = p.o1_stages_l;
+  const unsigned ring_e = smem_u32(smem_o1p) + (unsigned)colp_head<NP>();
+  const unsigned ring_l = ring_e + nE * SB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ncb = (p.Wd + 31) / 32;
+  const int task = blockIdx.x;
+  const int cb = task % ncb;
+  const int sy = (task / ncb) % p.o1_nseg_y;
+  const int b = task / (ncb * p.o1_nseg_y);
+  const int ys = sy * p.o1_seg_y, ye = min(ys + p.o1_seg_y, p.out_rows);
+  const int R = p.R;
+  const int zl = 2 * R + 1;                         // steps whose leaving sample is (virtual) zero
+  const int lead = (zl + kRPS - 1) / kRPS * kRPS;   // lead-in from zero state, whole stages
+  const int i0 = ys - lead;                         // window centre of step 0
+  const int ngroups = (lead + (ye - ys) + kRPS - 1) / kRPS;
+  const int gL0 = (zl + 1 - kRPS + kRPS - 1) / kRPS;   // first group with a real leaving row (k0 + kRPS - 1 >= zl)
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < nE; st++) {
+      o1_mbar_init_n(&sm.full_e[st], 1);
+      o1_mbar_init_n(&sm.empty_e[st], NP);
+    }
+    for (int st = 0; st < nL; st++) {
+      o1_mbar_init_n(&sm.full_l[st], 1);
+      o1_mbar_init_n(&sm.empty_l[st], NP);
+    }
+    for (int t = 0; t < 2; t++) {
+      o1_mbar_init_n(&sm.tile_full[t], NP);
+      o1_mbar_init_n(&sm.tile_free[t], NP);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();                                       // planes from k_row_o1
+
+  if (warp == NP) {                                 // ---- TMA producer (one elected lane)
+    if (lane == 0) {
+      unsigned long long pol_keep = 0, pol_drop = 0;
+      // entering rows are read again 2W+1 steps later as leaving rows: keep them in L2
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_drop));
+      const int x0 = cb * 32;
+      const int ybase = b * p.in_rows;
+      // kRPS rows starting at global row g0 (+1 per step) into dst
+      auto load = [&](unsigned dst, int g0, unsigned bar, unsigned long long pol) {
+        const int r0 = g0 - p.in_row0;
+        if (g0 >= 0 && g0 + kRPS <= p.H && r0 >= 0 && r0 + kRPS <= p.in_rows) {
+          tma_2d_hint(dst, &tmap4, x0, (ybase + r0) * NP, bar, pol);            // interior: one box
+        } else {
+#pragma unroll 1
+          for (int r = 0; r < kRPS; r++) {                                    // mirrored / clamped rows
+            const int rr = min(max(mirror(g0 + r, p.H) - p.in_row0, 0), p.in_rows - 1);
+            tma_2d_hint(dst + r * BOX, &tmap, x0, (ybase + rr) * NP, bar, pol);
+          }
+        }
+      };
+      // two rings, one issuing thread: entering groups run up to nE ahead of the consumers,
+      // leaving groups up to nL ahead (and never ahead of the entering stream)
+      int ge = 0, gl = gL0;
+      while (ge < ngroups || gl < ngroups) {
+        bool did = false;
+        if (ge < ngroups) {
+          const int st = ge % nE;
+          if (ge < nE || mbar_test(smem_u32(&sm.empty_e[st]), ((ge / nE) - 1) & 1)) {
+            const unsigned bar = smem_u32(&sm.full_e[st]);
+            o1_mbar_expect_tx(&sm.full_e[st], SB);
+            load(ring_e + st * SB, p.out_row0 + i0 + ge * kRPS + R + 1, bar, pol_keep);
+            ge++;
+            did = true;
+          }
+        }
+        if (gl < ngroups && gl < ge) {
+          const int j = gl - gL0, st = j % nL;
+          if (j < nL || mbar_test(smem_u32(&sm.empty_l[st]), ((j / nL) - 1) & 1)) {
+            const unsigned bar = smem_u32(&sm.full_l[st]);
+            o1_mbar_expect_tx(&sm.full_l[st], SB);
+            load(ring_l + st * SB, p.out_row0 + i0 + gl * kRPS - R, bar, pol_drop);
+            gl++;
+            did = true;
+          }
+        }
+        if (!did) __nanosleep(32);
+      }
+    }
+    return;
+  }
+
+  // ---- consumers: warp q = plane pair q, lane = column
+  const int q = warp;
+  const int x = cb * 32 + lane;
+  const bool xok = x < p.Wd;
+  const int xc = xok ? x : p.Wd - 1;
+  float2 S0 = make_float2(0.f, 0.f), Ep = S0, Lp = S0, S[kO1K - 1], D[kO1K - 1];
+#pragma unroll
+  for (int t = 0; t < kO1K - 1; t++) S[t] = D[t] = make_float2(0.f, 0.f);
+  // (plain C++ shared-memory accesses: ordered by the mbarrier asm's memory clobbers, free to be
+  // scheduled among themselves — the loads of a stage's kRPS rows issue back to back)
+  constexpr int BOXF = NP * 32, SBF = kRPS * BOXF;  // strides in float2
+  const float2* const my_e = reinterpret_cast<const float2*>(reinterpret_cast<const char*>(smem_o1p) +
+                                                            colp_head<NP>()) + q * 32 + lane;
+  const float2* const my_l = my_e + nE * SBF;
+  float2* const my_tile = &sm.tile[0][0][q][lane];
+  int ste = 0, stl = 0;
+  unsigned phe = 0, phl = 0;
+  auto advance = [&](float2 pe, float2 pl) {        // window i -> i+1
+    o1_update(p, S0, S, D, f2add(pe, Lp), f2add(Ep, pl), pe, pl);
+    Ep = pe;
+    Lp = pl;
+  };
+  // lead-in: whole groups, no output; leaving samples real from step zl on
+#pragma unroll 1
+  for (int g = 0; g * kRPS < lead; g++) {
+    mbar_wait_u32(smem_u32(&sm.full_e[ste]), phe);
+    const float2* se = my_e + ste * SBF;
+    const bool lv = g >= gL0;
+    const float2* sl = my_l + stl * SBF;
+    if (lv) mbar_wait_u32(smem_u32(&sm.full_l[stl]), phl);
+#pragma unroll
+    for (int r = 0; r < kRPS; r++) {
+      const float2 pe = se[r * BOXF];
+      const float2 pl = lv && g * kRPS + r >= zl ? sl[r * BOXF] : make_float2(0.f, 0.f);
+      advance(pe, pl);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      o1_mbar_arrive(&sm.empty_e[ste]);
+      if (lv) o1_mbar_arrive(&sm.empty_l[stl]);
+    }
+    if (++ste == nE) { ste = 0; phe ^= 1; }
+    if (lv && ++stl == nL) { stl = 0; phl ^= 1; }
+  }
+  float* const outp = p.out + b * p.out_img_stride + x;
+  unsigned nguard = 0;
+  const unsigned tf0 = smem_u32(&sm.tile_full[0]), tr0 = smem_u32(&sm.tile_free[0]);
+  // Blocks of kRPS output rows (one ring group each).  Block blk is filtered into tile buffer
+  // blk & 1 while block blk-1 is folded (eqs. 8-10) from the other buffer: warp q folds rows
+  // r = (q - blk') mod NP, + NP, ... (rotated per block, so the folds spread evenly over the
+  // warps), and the mbarriers tile_full / tile_free give every warp a block of slack.
+  const int nblk = (ye - ys + kRPS - 1) / kRPS;
+  float fo = 0.f;                                   // f at the first row this warp folds next
+#pragma unroll 1
+  for (int blk = 0; blk <= nblk; blk++) {
+    const int bs = ys + blk * kRPS;
+    const int pb = blk - 1;                         // block folded in this iteration
+    const int pbs = bs - kRPS;
+    const int pnb = pb >= 0 ? min(kRPS, ye - pbs) : 0;
+    const int r0 = pb >= 0 ? (q - pb % NP + NP) % NP : 0;
+    if (pb >= 0 && r0 < pnb) fo = __ldg(row_ptr(p, b, p.out_row0 + pbs + r0) + xc);   // used after the filtering
+    if (blk < nblk) {                               // ---- filter block blk into tile buffer blk & 1
+      const unsigned buf = blk & 1;
+      const int nb = min(kRPS, ye - bs);
+      if (blk >= 2) mbar_wait_u32(tr0 + 8 * buf, ((blk >> 1) - 1) & 1);   // block blk-2 folded
+      mbar_wait_u32(smem_u32(&sm.full_e[ste]), phe);
+      mbar_wait_u32(smem_u32(&sm.full_l[stl]), phl);
+      const float2* se = my_e + ste * SBF;
+      const float2* sl = my_l + stl * SBF;
+      float2* const tb = my_tile + buf * (kRPS * BOXF);
+      if (nb == kRPS) {
+#pragma unroll
+        for (int r = 0; r < kRPS; r++) {
+          const float2 pe = se[r * BOXF], pl = sl[r * BOXF];
+          tb[r * BOXF] = o1_output(p, S0, S);       // filtered pair q, row bs + r
+          advance(pe, pl);
+        }
+      } else {
+#pragma unroll 1
+        for (int r = 0; r < nb; r++) {
+          const float2 pe = se[r * BOXF], pl = sl[r * BOXF];
+          tb[r * BOXF] = o1_output(p, S0, S);
+          advance(pe, pl);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        o1_mbar_arrive(&sm.empty_e[ste]);
+        o1_mbar_arrive(&sm.empty_l[stl]);
+        o1_mbar_arrive(&sm.tile_full[buf]);
+      }
+      if (++ste == nE) { ste = 0; phe ^= 1; }
+      if (++stl == nL) { stl = 0; phl ^= 1; }
+    }
+    if (pb >= 0) {                                  // ---- fold block pb: eqs. (8)-(10)
+      const unsigned pbuf = pb & 1;
+      mbar_wait_u32(tf0 + 8 * pbuf, (pb >> 1) & 1);   // every warp's pair of block pb is in
+#pragma unroll 1
+      for (int row = r0, t = 0; row < pnb; row += NP, t++) {
+        const float f0 = t == 0 ? fo : __ldg(row_ptr(p, b, p.out_row0 + pbs + row) + xc);
+        const float a = p.raw ? 0.f : centre_a(p, f0);
+        const float a2 = a * a;
+        float2 Q2 = make_float2(0.f, 0.f), P2 = Q2, pw2 = make_float2(1.f, a);
+        float vprev = 0.f, out_raw = 0.f;
+        const float2* const rt = &sm.tile[pbuf][row][0][lane];
+#pragma unroll
+        for (int qq = 0; qq < NP; qq++) {
+          const float2 y = rt[qq * 32];
+          if (qq == 0) out_raw = y.x;
+          const float2 v = f2mul(p.chat2[qq], pw2);
+          Q2 = f2fma(v, y, Q2);
+          P2 = f2fma(make_float2(vprev, v.x), y, P2);
+          vprev = v.y;
+          pw2 = f2mul(pw2, f2s(a2));
+        }
+        const float Q = Q2.x + Q2.y, P = P2.x + P2.y;
+        if (xok) {
+          float o;
+          if (p.raw) {
+            o = out_raw;
+          } else if (Q > 0.f && isfinite(Q) && isfinite(P)) {
+            o = p.t_c + p.t_h * __fdividef(P, Q);          // eq. (10) + uncentring
+          } else {                                         // guard (R8)
+            o = fminf(fmaxf(f0, p.L), p.U);
+            nguard++;
+          }
+          outp[(long long)(pbs + row) * p.Wd] = o;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) o1_mbar_arrive(&sm.tile_free[pbuf]);
+    }
+  }
+  count_guarded(p.fallback, 0xffffffffu, nguard);
+}
+
 // ------------------------------------------------------------------ dispatch
 
 namespace {
 
 // TMA descriptor of the O(1) plane buffer [B*rows*NP][Wd] (8-byte elements), box 32 x NP.
-bool make_o1_plane_map(CUtensorMap* map, const KParams& p) {
+bool make_o1_plane_map(CUtensorMap* map, const KParams& p, int rows_per_box = 1) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -485,7 +850,7 @@ bool make_o1_plane_map(CUtensorMap* map, const KParams& p) {
   }
   const cuuint64_t dims[2] = {(cuuint64_t)p.Wd, (cuuint64_t)p.B * p.in_rows * p.NP};
   const cuuint64_t strides[1] = {(cuuint64_t)p.Wd * 8};
-  const cuuint32_t box[2] = {32, (cuuint32_t)p.NP};
+  const cuuint32_t box[2] = {32, (cuuint32_t)(p.NP * rows_per_box)};
   const cuuint32_t estr[2] = {1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_INT64, 2, (void*)p.planes, dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -524,6 +889,57 @@ cudaError_t launch_col(const KParams& p0, cudaStream_t s) {
   return launch_k(kern, dim3(grid), dim3(32 * kO1Warps), smem, s, p.ev[1] == nullptr, map, p);
 }
 
+// CTAs per SM for k_col_o1p: bounds the GPU's in-flight leaving-row windows (CTAs x 148 x
+// NP x 32 x (2W+1) x 8 B) so they stay L2-resident; GC_O1P_CTAS overrides (development A/B).
+int o1p_ctas_per_sm() {
+  static const int v = [] {
+    const char* e = std::getenv("GC_O1P_CTAS");
+    const int n = e ? std::atoi(e) : 2;
+    return n < 1 ? 1 : (n > 8 ? 8 : n);
+  }();
+  return v;
+}
+
+template <int NP>
+cudaError_t launch_colp(const KParams& p0, cudaStream_t s) {
+  CUtensorMap map, map4;
+  std::memset(&map, 0, sizeof(map));
+  std::memset(&map4, 0, sizeof(map4));
+  if (!make_o1_plane_map(&map, p0) || !make_o1_plane_map(&map4, p0, kRPS)) return cudaErrorNotSupported;
+  auto kern = k_col_o1p<NP>;
+  // dynamic shared memory padded so that at most o1p_ctas_per_sm() CTAs fit on an SM
+  int dev = 0, smem_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  const int ctas = o1p_ctas_per_sm();
+  // ring depth: every stage the CTA's share of the SM's shared memory holds (a deep ring is what
+  // hides the TMA latency: each step's compute is short), NP <= stages <= kPDMax
+  const size_t cap = std::min<size_t>((size_t)(smem_sm > 0 ? smem_sm : 233472) / ctas - 1024, 227 * 1024);
+  const int nst = std::max(4, (int)((cap - colp_head<NP>()) / colp_stage<NP>()));
+  // leaving rows hit L2: a short ring (a quarter of the stages, at least 2) is enough
+  int nL = std::max(2, nst / 4);
+  if (const char* env = std::getenv("GC_O1P_NL")) nL = std::max(1, std::atoi(env));
+  const int nE = std::max(2, std::min(nst - nL, kPDMax));
+  nL = std::min(nL, kPDMax);
+  const size_t smem = colp_head<NP>() + (size_t)(nE + nL) * colp_stage<NP>();
+  static std::atomic<unsigned long long> ready{0};   // opt in to the largest ring once per device
+  const cudaError_t e = once_per_device(ready, [&]() {
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  if (e != cudaSuccess) return e;
+  int blocks = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, 32 * (NP + 1), smem) != cudaSuccess || blocks < 1)
+    blocks = 1;
+  KParams p = p0;
+  p.o1_stages = nE;
+  p.o1_stages_l = nL;
+
+  const long long ncb = (p.Wd + 31) / 32;
+  pick_segments(p.out_rows, ncb * p.B, 2 * p.R + 1, (long long)blocks * p.num_sms, 1, p.o1_seg_y, p.o1_nseg_y);
+  const long long nt = ncb * p.o1_nseg_y * p.B;
+  return launch_k(kern, dim3((unsigned)nt), dim3(32 * (NP + 1)), smem, s, p.ev[1] == nullptr, map, map4, p);
+}
+
 template <int G, int LO, int HI>
 cudaError_t launch_col_g(const KParams& p, int npg, cudaStream_t s) {
   if constexpr (LO > HI) {
@@ -559,7 +975,25 @@ cudaError_t launch_o1_two_pass(const KParams& p0, cudaStream_t s) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (p.ev[1]) cudaEventRecord(p.ev[1], s);
-  // column pass: G lanes per column, NPG = ceil(NP / G) <= 5 pairs per lane
+  // column pass: the pair-parallel kernel (NP <= 8, even width: TMA boxes), else G lanes per
+  // column with NPG = ceil(NP / G) pairs per lane
+  static const bool legacy = std::getenv("GC_O1_COL_LEGACY") != nullptr;   // A/B switch (development)
+  if (!legacy && p.NP <= 8 && (p.Wd & 1) == 0) {
+    switch (p.NP) {
+      case 1: e = launch_colp<1>(p, s); break;
+      case 2: e = launch_colp<2>(p, s); break;
+      case 3: e = launch_colp<3>(p, s); break;
+      case 4: e = launch_colp<4>(p, s); break;
+      case 5: e = launch_colp<5>(p, s); break;
+      case 6: e = launch_colp<6>(p, s); break;
+      case 7: e = launch_colp<7>(p, s); break;
+      default: e = launch_colp<8>(p, s); break;
+    }
+    if (e != cudaErrorNotSupported) {
+      if (p.ev[2]) cudaEventRecord(p.ev[2], s);
+      return e;
+    }
+  }
   int G, npg;
   o1_col_split(p.NP, G, npg);
   switch (G) {

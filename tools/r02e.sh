@@ -1,0 +1,7 @@
+set -u
+O=gpurun_out/r02e; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_operator.py tests/test_gpu_parity.py -m gpu -q -x > $O/pytest.log 2>&1; echo "pytest exit $?"; tail -3 $O/pytest.log
+TAILN=1 tools/gpu_ab_env.sh r02e "c5 --op 2 --reps 5" "GC_O1_COL_LEGACY=1" "GC_O1P_L2HINT=0 GC_O1P_CTAS=2" "GC_O1P_L2HINT=1 GC_O1P_CTAS=2" "GC_O1P_L2HINT=1 GC_O1P_CTAS=3" "GC_O1P_L2HINT=0 GC_O1P_CTAS=3"
+TAILN=3 tools/gpu_ab_env.sh r02e "c3 --op 2 --sigma-s 2 10 40 --reps 10" "GC_O1_COL_LEGACY=1" "GC_O1P_CTAS=2" "GC_O1P_CTAS=3"
+CMD="python tools/time_ops.py c5 --H 8192 --W 8192 --op 2 --reps 1"
+$CMD > $O/plain.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_(row|col)_o1" -s 2 -c 2 -o $O/prof $CMD > $O/ncu.log 2>&1; echo "ncu exit $?"

@@ -73,7 +73,7 @@ struct KParams {
   int o1_seg_x, o1_nseg_x;         // row pass: x-segment length (multiple of 32) and count
   int o1_seg_y, o1_nseg_y;         // column pass: y-segment length and count
   int o1_groups;                   // row pass: plane-pair groups (<= 4 pairs each)
-  int o1_stages, o1_stages_l;      // pair-parallel column pass: entering / leaving TMA ring stages
+  int o1_stages;                   // pair-parallel column pass: TMA ring stages
   int raw;                         // 1: eq. (7) of f itself (gc_gaussian): pair 0 = (f, 0), out = Fbar_0
   // Deriche-class recursive operator (gc_deriche.cu; GC_OP_DERICHE): two 2nd-order sections per
   // direction, 1/Z folded into b0, b1, c1, c2

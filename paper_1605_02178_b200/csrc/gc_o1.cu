@@ -524,24 +524,23 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const __grid_constant_
 // stay in L2 and the leaving rows are not re-read from HBM (k_col_o1 at c5: ~1200 resident
 // warps x 174 KB = 206 MB, 123 B/px of DRAM traffic instead of 64; profiles/r01_ncu_full_o1_c5.txt).
 
-constexpr int kPDMax = 48;       // ring stages per direction (at most)
+constexpr int kPDMax = 48;       // ring stages (at most)
 constexpr int kRPS = 4;          // image rows per ring stage: one [4 NP x 32] TMA box per direction in the
                                  // interior (per-row boxes where the rows are mirrored or clamped)
+constexpr int kPRB = 8;          // output rows per fold block (two ring stages: static ring offsets)
 
-// Shared memory: this head, then the entering ring (nE stages) and the leaving ring (nL stages),
-// each stage kRPS rows x [NP pairs x 32 columns] float2.  Entering rows come from HBM (first
-// touch) and get the deep ring; leaving rows are the entering rows of 2W+1 steps earlier, kept in
-// L2 by the evict_last hint, and get a short ring.
+// Shared memory: this head, then the ring of nst stages, each = kRPS entering rows followed by
+// kRPS leaving rows, a row = [NP pairs x 32 columns] float2.
 template <int NP>
 struct alignas(1024) ColPSmem {
-  unsigned long long full_e[kPDMax], empty_e[kPDMax], full_l[kPDMax], empty_l[kPDMax];
+  unsigned long long full[kPDMax], empty[kPDMax];
   unsigned long long tile_full[2], tile_free[2];   // per tile buffer: all NP warps wrote / folded it
-  float2 tile[2][kRPS][NP][32];  // [buffer][row in block][pair][column]
+  float2 tile[2][kPRB][NP][32];  // [buffer][row in block][pair][column]
 };
 template <int NP>
 __host__ __device__ constexpr size_t colp_head() { return (sizeof(ColPSmem<NP>) + 1023) / 1024 * 1024; }
 template <int NP>
-__host__ __device__ constexpr size_t colp_stage() { return (size_t)kRPS * NP * 32u * sizeof(float2); }
+__host__ __device__ constexpr size_t colp_stage() { return 2u * kRPS * NP * 32u * sizeof(float2); }
 
 __device__ __forceinline__ void o1_mbar_init_n(unsigned long long* bar, unsigned n) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(bar);
@@ -566,19 +565,6 @@ __device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned phase) {
       "}\n" ::"r"(bar),
       "r"(phase)
       : "memory");
-}
-__device__ __forceinline__ bool mbar_test(unsigned bar, unsigned phase) {
-  unsigned ok;
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, P1;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(bar), "r"(phase)
-      : "memory");
-  return ok != 0;
 }
 __device__ __forceinline__ float2 lds64(unsigned a) {
   float2 v;
@@ -610,10 +596,10 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
   extern __shared__ __align__(1024) float4 smem_o1p[];
   ColPSmem<NP>& sm = *reinterpret_cast<ColPSmem<NP>*>(smem_o1p);
   constexpr unsigned BOX = NP * 32u * 8u;           // one image row: [NP pairs x 32 columns]
-  constexpr unsigned SB = kRPS * BOX;               // one stage (kRPS rows)
-  const int nE = p.o1_stages, nL = p.o1_stages_l;
-  const unsigned ring_e = smem_u32(smem_o1p) + (unsigned)colp_head<NP>();
-  const unsigned ring_l = ring_e + nE * SB;
+  constexpr unsigned DIR = kRPS * BOX;              // one direction of a stage (kRPS rows)
+  constexpr unsigned SB = 2u * DIR;                 // stage: entering rows, then leaving rows
+  const int nst = p.o1_stages;
+  const unsigned ring = smem_u32(smem_o1p) + (unsigned)colp_head<NP>();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncb = (p.Wd + 31) / 32;
   const int task = blockIdx.x;
@@ -626,15 +612,10 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
   const int lead = (zl + kRPS - 1) / kRPS * kRPS;   // lead-in from zero state, whole stages
   const int i0 = ys - lead;                         // window centre of step 0
   const int ngroups = (lead + (ye - ys) + kRPS - 1) / kRPS;
-  const int gL0 = (zl + 1 - kRPS + kRPS - 1) / kRPS;   // first group with a real leaving row (k0 + kRPS - 1 >= zl)
   if (threadIdx.x == 0) {
-    for (int st = 0; st < nE; st++) {
-      o1_mbar_init_n(&sm.full_e[st], 1);
-      o1_mbar_init_n(&sm.empty_e[st], NP);
-    }
-    for (int st = 0; st < nL; st++) {
-      o1_mbar_init_n(&sm.full_l[st], 1);
-      o1_mbar_init_n(&sm.empty_l[st], NP);
+    for (int st = 0; st < nst; st++) {
+      o1_mbar_init_n(&sm.full[st], 1);
+      o1_mbar_init_n(&sm.empty[st], NP);
     }
     for (int t = 0; t < 2; t++) {
       o1_mbar_init_n(&sm.tile_full[t], NP);
@@ -666,32 +647,18 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
           }
         }
       };
-      // two rings, one issuing thread: entering groups run up to nE ahead of the consumers,
-      // leaving groups up to nL ahead (and never ahead of the entering stream)
-      int ge = 0, gl = gL0;
-      while (ge < ngroups || gl < ngroups) {
-        bool did = false;
-        if (ge < ngroups) {
-          const int st = ge % nE;
-          if (ge < nE || mbar_test(smem_u32(&sm.empty_e[st]), ((ge / nE) - 1) & 1)) {
-            const unsigned bar = smem_u32(&sm.full_e[st]);
-            o1_mbar_expect_tx(&sm.full_e[st], SB);
-            load(ring_e + st * SB, p.out_row0 + i0 + ge * kRPS + R + 1, bar, pol_keep);
-            ge++;
-            did = true;
-          }
-        }
-        if (gl < ngroups && gl < ge) {
-          const int j = gl - gL0, st = j % nL;
-          if (j < nL || mbar_test(smem_u32(&sm.empty_l[st]), ((j / nL) - 1) & 1)) {
-            const unsigned bar = smem_u32(&sm.full_l[st]);
-            o1_mbar_expect_tx(&sm.full_l[st], SB);
-            load(ring_l + st * SB, p.out_row0 + i0 + gl * kRPS - R, bar, pol_drop);
-            gl++;
-            did = true;
-          }
-        }
-        if (!did) __nanosleep(32);
+      int st = 0;
+      unsigned ph = 0;
+      for (int g = 0; g < ngroups; g++) {
+        if (g >= nst) mbar_wait_u32(smem_u32(&sm.empty[st]), ph ^ 1);
+        const int k0 = g * kRPS;                    // first step of the group
+        const bool leave = k0 + kRPS - 1 >= zl;     // some step of the group has a real leaving row
+        const unsigned bar = smem_u32(&sm.full[st]);
+        o1_mbar_expect_tx(&sm.full[st], leave ? SB : DIR);
+        const unsigned dst = ring + st * SB;
+        load(dst, p.out_row0 + i0 + k0 + R + 1, bar, pol_keep);
+        if (leave) load(dst + DIR, p.out_row0 + i0 + k0 - R, bar, pol_drop);
+        if (++st == nst) { st = 0; ph ^= 1; }
       }
     }
     return;
@@ -707,96 +674,96 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
   for (int t = 0; t < kO1K - 1; t++) S[t] = D[t] = make_float2(0.f, 0.f);
   // (plain C++ shared-memory accesses: ordered by the mbarrier asm's memory clobbers, free to be
   // scheduled among themselves — the loads of a stage's kRPS rows issue back to back)
-  constexpr int BOXF = NP * 32, SBF = kRPS * BOXF;  // strides in float2
-  const float2* const my_e = reinterpret_cast<const float2*>(reinterpret_cast<const char*>(smem_o1p) +
-                                                            colp_head<NP>()) + q * 32 + lane;
-  const float2* const my_l = my_e + nE * SBF;
+  constexpr int BOXF = NP * 32, DIRF = kRPS * BOXF, SBF = 2 * DIRF;   // strides in float2
+  const float2* const my_ring = reinterpret_cast<const float2*>(reinterpret_cast<const char*>(smem_o1p) +
+                                                               colp_head<NP>()) + q * 32 + lane;
   float2* const my_tile = &sm.tile[0][0][q][lane];
-  int ste = 0, stl = 0;
-  unsigned phe = 0, phl = 0;
+  int st = 0;
+  unsigned ph = 0;
+  const float2* sbase = my_ring;                    // this lane's sample in the current stage
   auto advance = [&](float2 pe, float2 pl) {        // window i -> i+1
     o1_update(p, S0, S, D, f2add(pe, Lp), f2add(Ep, pl), pe, pl);
     Ep = pe;
     Lp = pl;
   };
-  // lead-in: whole groups, no output; leaving samples real from step zl on
+  auto acquire = [&]() {
+    mbar_wait_u32(smem_u32(&sm.full[st]), ph);
+    sbase = my_ring + st * SBF;
+  };
+  auto release = [&]() {
+    __syncwarp();
+    if (lane == 0) o1_mbar_arrive(&sm.empty[st]);
+    if (++st == nst) { st = 0; ph ^= 1; }
+  };
+  // lead-in: whole stages, no output; leaving samples real from step zl on
 #pragma unroll 1
-  for (int g = 0; g * kRPS < lead; g++) {
-    mbar_wait_u32(smem_u32(&sm.full_e[ste]), phe);
-    const float2* se = my_e + ste * SBF;
-    const bool lv = g >= gL0;
-    const float2* sl = my_l + stl * SBF;
-    if (lv) mbar_wait_u32(smem_u32(&sm.full_l[stl]), phl);
+  for (int k0 = 0; k0 < lead; k0 += kRPS) {
+    acquire();
 #pragma unroll
     for (int r = 0; r < kRPS; r++) {
-      const float2 pe = se[r * BOXF];
-      const float2 pl = lv && g * kRPS + r >= zl ? sl[r * BOXF] : make_float2(0.f, 0.f);
+      const float2 pe = sbase[r * BOXF];
+      const float2 pl = k0 + r >= zl ? sbase[DIRF + r * BOXF] : make_float2(0.f, 0.f);
       advance(pe, pl);
     }
-    __syncwarp();
-    if (lane == 0) {
-      o1_mbar_arrive(&sm.empty_e[ste]);
-      if (lv) o1_mbar_arrive(&sm.empty_l[stl]);
-    }
-    if (++ste == nE) { ste = 0; phe ^= 1; }
-    if (lv && ++stl == nL) { stl = 0; phl ^= 1; }
+    release();
   }
   float* const outp = p.out + b * p.out_img_stride + x;
   unsigned nguard = 0;
   const unsigned tf0 = smem_u32(&sm.tile_full[0]), tr0 = smem_u32(&sm.tile_free[0]);
-  // Blocks of kRPS output rows (one ring group each).  Block blk is filtered into tile buffer
-  // blk & 1 while block blk-1 is folded (eqs. 8-10) from the other buffer: warp q folds rows
-  // r = (q - blk') mod NP, + NP, ... (rotated per block, so the folds spread evenly over the
-  // warps), and the mbarriers tile_full / tile_free give every warp a block of slack.
-  const int nblk = (ye - ys + kRPS - 1) / kRPS;
-  float fo = 0.f;                                   // f at the first row this warp folds next
+  // Blocks of kPRB output rows.  Block blk is filtered into tile buffer blk & 1 while block blk-1 is
+  // folded (eqs. 8-10) from the other buffer: warp q folds rows r = (q - blk') mod NP, + NP, ...
+  // (rotated per block, so the kPRB - NP extra rows spread over the warps), and the mbarriers
+  // tile_full / tile_free give every warp a block of slack instead of a per-block barrier.
+  const int nblk = (ye - ys + kPRB - 1) / kPRB;
+  float fo = 0.f, fo2 = 0.f;                        // f at the first two rows this warp folds next
 #pragma unroll 1
   for (int blk = 0; blk <= nblk; blk++) {
-    const int bs = ys + blk * kRPS;
+    const int bs = ys + blk * kPRB;
     const int pb = blk - 1;                         // block folded in this iteration
-    const int pbs = bs - kRPS;
-    const int pnb = pb >= 0 ? min(kRPS, ye - pbs) : 0;
+    const int pbs = bs - kPRB;
+    const int pnb = pb >= 0 ? min(kPRB, ye - pbs) : 0;
     const int r0 = pb >= 0 ? (q - pb % NP + NP) % NP : 0;
-    if (pb >= 0 && r0 < pnb) fo = __ldg(row_ptr(p, b, p.out_row0 + pbs + r0) + xc);   // used after the filtering
+    if (pb >= 0) {                                  // f for the fold below, loaded before the filtering
+      fo = r0 < pnb ? __ldg(row_ptr(p, b, p.out_row0 + pbs + r0) + xc) : 0.f;
+      fo2 = r0 + NP < pnb ? __ldg(row_ptr(p, b, p.out_row0 + pbs + r0 + NP) + xc) : 0.f;
+    }
     if (blk < nblk) {                               // ---- filter block blk into tile buffer blk & 1
       const unsigned buf = blk & 1;
-      const int nb = min(kRPS, ye - bs);
+      const int nb = min(kPRB, ye - bs);
       if (blk >= 2) mbar_wait_u32(tr0 + 8 * buf, ((blk >> 1) - 1) & 1);   // block blk-2 folded
-      mbar_wait_u32(smem_u32(&sm.full_e[ste]), phe);
-      mbar_wait_u32(smem_u32(&sm.full_l[stl]), phl);
-      const float2* se = my_e + ste * SBF;
-      const float2* sl = my_l + stl * SBF;
-      float2* const tb = my_tile + buf * (kRPS * BOXF);
-      if (nb == kRPS) {
+      float2* const tb = my_tile + buf * (kPRB * BOXF);
+      if (nb == kPRB) {
 #pragma unroll
-        for (int r = 0; r < kRPS; r++) {
-          const float2 pe = se[r * BOXF], pl = sl[r * BOXF];
-          tb[r * BOXF] = o1_output(p, S0, S);       // filtered pair q, row bs + r
-          advance(pe, pl);
+        for (int h = 0; h < kPRB / kRPS; h++) {
+          acquire();
+#pragma unroll
+          for (int r = 0; r < kRPS; r++) {
+            const float2 pe = sbase[r * BOXF], pl = sbase[DIRF + r * BOXF];
+            tb[(h * kRPS + r) * BOXF] = o1_output(p, S0, S);   // filtered pair q, row bs + h kRPS + r
+            advance(pe, pl);
+          }
+          release();
         }
       } else {
 #pragma unroll 1
-        for (int r = 0; r < nb; r++) {
-          const float2 pe = se[r * BOXF], pl = sl[r * BOXF];
-          tb[r * BOXF] = o1_output(p, S0, S);
+        for (int jj = 0; jj < nb; jj++) {
+          const int r = jj % kRPS;
+          if (r == 0) acquire();
+          const float2 pe = sbase[r * BOXF], pl = sbase[DIRF + r * BOXF];
+          tb[jj * BOXF] = o1_output(p, S0, S);
           advance(pe, pl);
+          if (r == kRPS - 1 || jj == nb - 1) release();
         }
       }
       __syncwarp();
-      if (lane == 0) {
-        o1_mbar_arrive(&sm.empty_e[ste]);
-        o1_mbar_arrive(&sm.empty_l[stl]);
-        o1_mbar_arrive(&sm.tile_full[buf]);
-      }
-      if (++ste == nE) { ste = 0; phe ^= 1; }
-      if (++stl == nL) { stl = 0; phl ^= 1; }
+      if (lane == 0) o1_mbar_arrive(&sm.tile_full[buf]);
     }
     if (pb >= 0) {                                  // ---- fold block pb: eqs. (8)-(10)
       const unsigned pbuf = pb & 1;
       mbar_wait_u32(tf0 + 8 * pbuf, (pb >> 1) & 1);   // every warp's pair of block pb is in
 #pragma unroll 1
       for (int row = r0, t = 0; row < pnb; row += NP, t++) {
-        const float f0 = t == 0 ? fo : __ldg(row_ptr(p, b, p.out_row0 + pbs + row) + xc);
+        const float f0 = t == 0 ? fo : t == 1 ? fo2 : __ldg(row_ptr(p, b, p.out_row0 + pbs + row) + xc);
         const float a = p.raw ? 0.f : centre_a(p, f0);
         const float a2 = a * a;
         float2 Q2 = make_float2(0.f, 0.f), P2 = Q2, pw2 = make_float2(1.f, a);
@@ -894,7 +861,7 @@ cudaError_t launch_col(const KParams& p0, cudaStream_t s) {
 int o1p_ctas_per_sm() {
   static const int v = [] {
     const char* e = std::getenv("GC_O1P_CTAS");
-    const int n = e ? std::atoi(e) : 2;
+    const int n = e ? std::atoi(e) : 3;
     return n < 1 ? 1 : (n > 8 ? 8 : n);
   }();
   return v;
@@ -915,13 +882,10 @@ cudaError_t launch_colp(const KParams& p0, cudaStream_t s) {
   // ring depth: every stage the CTA's share of the SM's shared memory holds (a deep ring is what
   // hides the TMA latency: each step's compute is short), NP <= stages <= kPDMax
   const size_t cap = std::min<size_t>((size_t)(smem_sm > 0 ? smem_sm : 233472) / ctas - 1024, 227 * 1024);
-  const int nst = std::max(4, (int)((cap - colp_head<NP>()) / colp_stage<NP>()));
-  // leaving rows hit L2: a short ring (a quarter of the stages, at least 2) is enough
-  int nL = std::max(2, nst / 4);
-  if (const char* env = std::getenv("GC_O1P_NL")) nL = std::max(1, std::atoi(env));
-  const int nE = std::max(2, std::min(nst - nL, kPDMax));
-  nL = std::min(nL, kPDMax);
-  const size_t smem = colp_head<NP>() + (size_t)(nE + nL) * colp_stage<NP>();
+  int nst = (int)((cap - colp_head<NP>()) / colp_stage<NP>());
+  if (const char* env = std::getenv("GC_O1P_STAGES")) nst = std::min(nst, std::atoi(env));
+  nst = std::max(kPRB / kRPS, std::min(nst, kPDMax));   // (>= one fold block: no producer starvation)
+  const size_t smem = colp_head<NP>() + (size_t)nst * colp_stage<NP>();
   static std::atomic<unsigned long long> ready{0};   // opt in to the largest ring once per device
   const cudaError_t e = once_per_device(ready, [&]() {
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -931,8 +895,7 @@ cudaError_t launch_colp(const KParams& p0, cudaStream_t s) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, 32 * (NP + 1), smem) != cudaSuccess || blocks < 1)
     blocks = 1;
   KParams p = p0;
-  p.o1_stages = nE;
-  p.o1_stages_l = nL;
+  p.o1_stages = nst;
 
   const long long ncb = (p.Wd + 31) / 32;
   pick_segments(p.out_rows, ncb * p.B, 2 * p.R + 1, (long long)blocks * p.num_sms, 1, p.o1_seg_y, p.o1_nseg_y);
@@ -954,13 +917,14 @@ cudaError_t launch_col_g(const KParams& p, int npg, cudaStream_t s) {
 
 cudaError_t launch_o1_two_pass(const KParams& p0, cudaStream_t s) {
   // row pass: warp tasks = 32 rows x one x-segment x one group of <= 4 plane pairs
+  auto row_kern = k_row_o1;
   const size_t smem_r = (size_t)kO1Warps * sizeof(RowO1Smem);
   static std::atomic<unsigned long long> ready{0};
   static std::atomic<long long> resident_r{1};
   {
     const cudaError_t e = once_per_device(ready, [&]() {
-      cudaError_t r = cudaFuncSetAttribute(k_row_o1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r);
-      if (r == cudaSuccess) resident_r.store(o1_resident_warps(k_row_o1, smem_r, p0.num_sms));
+      cudaError_t r = cudaFuncSetAttribute(row_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r);
+      if (r == cudaSuccess) resident_r.store(o1_resident_warps(row_kern, smem_r, p0.num_sms));
       return r;
     });
     if (e != cudaSuccess) return e;
@@ -971,7 +935,7 @@ cudaError_t launch_o1_two_pass(const KParams& p0, cudaStream_t s) {
   pick_segments(p.Wd, nrb * p.o1_groups * p.B, 2 * p.R + 1, resident_r.load(), 32, p.o1_seg_x, p.o1_nseg_x);
   const long long ntr = nrb * p.o1_nseg_x * p.o1_groups * p.B;
   if (p.ev[0]) cudaEventRecord(p.ev[0], s);
-  k_row_o1<<<(unsigned)((ntr + kO1Warps - 1) / kO1Warps), 32 * kO1Warps, smem_r, s>>>(p);
+  row_kern<<<(unsigned)((ntr + kO1Warps - 1) / kO1Warps), 32 * kO1Warps, smem_r, s>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (p.ev[1]) cudaEventRecord(p.ev[1], s);

@@ -274,6 +274,22 @@ gc_status gc_filter_band(const float* band, int H_band, int W, int H_global, int
                          const gc_params* p, float* out, void* comm, void* stream);
 
 /*
+ * gc_debug_oob_count — bounds-check builds only (libgc_check.so, compiled with
+ * -DGC_BOUNDS_CHECK: every global-memory access of the kernels is checked against the call's
+ * input segments, plane / scratch buffer, output and taps, since compute-sanitizer is not
+ * available on the B200 pool).  Synchronises the device, stores the number of out-of-bounds
+ * accesses counted since the last call in *count and resets it.  GC_ERANGE in the product
+ * library (no checks compiled in), GC_EINVAL if count is NULL.
+ */
+gc_status gc_debug_oob_count(unsigned long long* count);
+
+/* gc_debug_oob_selftest — bounds-check builds only: launches a kernel that checks one address
+   just past a scratch region and one inside it (no memory access), so that the next
+   gc_debug_oob_count reports exactly 1 — the positive control of the checks.  GC_ERANGE in the
+   product library. */
+gc_status gc_debug_oob_selftest(void);
+
+/*
  * gc_scratch_trim — release reserved stream-ordered scratch of libgc's private memory pool
  * of the current device back to the driver, keeping at most keep_bytes reserved.  libgc
  * never uses the device's default pool; by default its pool keeps freed scratch (the c5

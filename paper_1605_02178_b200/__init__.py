@@ -18,7 +18,7 @@ __all__ = [
     "GCError", "lib", "coeffs", "bilateral", "bilateral_batch", "bilateral_c", "filter",
     "filter_host", "filter_window", "band_plan", "Comm", "bilateral_band", "version",
     "OP_AUTO", "OP_FIR", "OP_O1", "OP_DERICHE", "gaussian", "operator_taps", "bilateral_direct",
-    "band_exchange_plan", "filter_band", "scratch_trim",
+    "band_exchange_plan", "filter_band", "scratch_trim", "debug_oob_count", "debug_oob_selftest",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -87,6 +87,8 @@ def _lib():
         L.gc_comm_wait.argtypes = [vp, vp, d]
         L.gc_filter_band.argtypes = [vp, i, i, i, i, ctypes.POINTER(_Params), vp, vp, vp]
         L.gc_scratch_trim.argtypes = [ctypes.c_size_t]
+        L.gc_debug_oob_count.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+        L.gc_debug_oob_selftest.argtypes = []
         L.gc_comm_unique_id.argtypes = [ctypes.c_char_p]
         L.gc_comm_init.argtypes = [i, i, ctypes.c_char_p, ctypes.POINTER(vp)]
         L.gc_comm_destroy.argtypes = [vp]
@@ -95,7 +97,7 @@ def _lib():
                      "gc_filter_host", "gc_filter_window", "gc_band_plan", "gc_comm_unique_id",
                      "gc_comm_init", "gc_comm_destroy", "gc_bilateral_band", "gc_gaussian", "gc_operator_taps",
                      "gc_bilateral_direct", "gc_band_exchange_plan", "gc_comm_wait", "gc_filter_band",
-                     "gc_scratch_trim"]:
+                     "gc_scratch_trim", "gc_debug_oob_count", "gc_debug_oob_selftest"]:
             getattr(L, name).restype = ctypes.c_int
         _LIB = L
     return _LIB
@@ -416,3 +418,16 @@ def scratch_trim(keep_bytes: int = 0, device=None):
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     with _on_device(dev):
         _check(_lib().gc_scratch_trim(int(keep_bytes)), "gc_scratch_trim")
+
+
+def debug_oob_count():
+    """gc_debug_oob_count: out-of-bounds device accesses counted since the last call (bounds-check
+    build libgc_check.so only; raises GCError(GC_ERANGE) on the product library)."""
+    c = ctypes.c_ulonglong()
+    _check(_lib().gc_debug_oob_count(ctypes.byref(c)), "gc_debug_oob_count")
+    return int(c.value)
+
+
+def debug_oob_selftest():
+    """gc_debug_oob_selftest: positive control — the next debug_oob_count() returns exactly 1."""
+    _check(_lib().gc_debug_oob_selftest(), "gc_debug_oob_selftest")

@@ -173,6 +173,23 @@ cudaMemPool_t scratch_pool() {
   return pools[dev];
 }
 
+// GC_BOUNDS_CHECK builds: a per-device counter of out-of-bounds device accesses (gc_device.cuh
+// GC_CHK); nullptr in the product library.
+unsigned long long* oob_counter() {
+#ifdef GC_BOUNDS_CHECK
+  static std::mutex mu;
+  static unsigned long long* ctr[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ctr[dev] && cudaMalloc((void**)&ctr[dev], sizeof(unsigned long long)) == cudaSuccess)
+    cudaMemset(ctr[dev], 0, sizeof(unsigned long long));
+  return ctr[dev];
+#else
+  return nullptr;
+#endif
+}
+
 cudaError_t scratch_alloc(void** ptr, size_t bytes, cudaStream_t s) {
   cudaMemPool_t pl = scratch_pool();
   if (!pl) return cudaErrorInitializationError;
@@ -253,6 +270,8 @@ gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) 
   cudaError_t e = scratch_alloc((void**)&planes, plane_elems * k.B * elem + 256 + scratch_elems * elem, s);
   if (e != cudaSuccess) return cuda_status(e);
   k.counters = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(planes) + plane_elems * k.B * elem);
+  k.planes_bytes = plane_elems * k.B * elem + 256 + scratch_elems * elem;
+  k.oob = oob_counter();
   k.scratch = scratch_elems ? reinterpret_cast<float2*>(reinterpret_cast<char*>(k.counters) + 256) : nullptr;
   if (k.fp64 || (op == GC_OP_FIR && k.R > kMaxTemplW)) {
     // taps for the runtime-radius kernels: (k_m, k_m) fp32 pairs, or k_m in binary64
@@ -307,7 +326,40 @@ const char* gc_status_string(gc_status s) {
   return "GC_?: unknown status";
 }
 
-const char* gc_version(void) { return "gc 0.2.0 sm_100a"; }
+const char* gc_version(void) {
+#ifdef GC_BOUNDS_CHECK
+  return "gc 0.2.0 sm_100a +bounds-check";
+#else
+  return "gc 0.2.0 sm_100a";
+#endif
+}
+
+gc_status gc_debug_oob_count(unsigned long long* count) {
+  if (!count) return GC_EINVAL;
+  unsigned long long* c = oob_counter();
+  if (!c) return GC_ERANGE;                       // not a GC_BOUNDS_CHECK build
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(count, c, sizeof(*count), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemset(c, 0, sizeof(*count));
+  return cuda_status(e);
+}
+
+gc_status gc_debug_oob_selftest(void) {
+  unsigned long long* c = oob_counter();
+  if (!c) return GC_ERANGE;                       // not a GC_BOUNDS_CHECK build
+  KParams k;
+  std::memset(&k, 0, sizeof(k));
+  float2* buf = nullptr;
+  cudaError_t e = cudaMalloc((void**)&buf, 4096);
+  if (e != cudaSuccess) return cuda_status(e);
+  k.planes = buf;
+  k.planes_bytes = 4096;
+  k.oob = c;
+  e = launch_oob_selftest(k, nullptr);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  cudaFree(buf);
+  return cuda_status(e);
+}
 
 gc_status gc_scratch_trim(size_t keep_bytes) {
   cudaMemPool_t pl = scratch_pool();

@@ -174,7 +174,10 @@ __global__ void __launch_bounds__(32 * kDrWarps) k_row_dr(const KParams p) {
   // issued before the current group's recursions)
   auto load8 = [&](int c, float (&v)[8]) {
 #pragma unroll
-    for (int i = 0; i < 8; i++) v[i] = __ldg(src + mirror(c + i, n));
+    for (int i = 0; i < 8; i++) {
+      GC_CHK(p, src + mirror(c + i, n), 4);
+      v[i] = __ldg(src + mirror(c + i, n));
+    }
   };
 
   // ---- causal sweep, padded coordinates c in [cs0, x1), cs0 = max(x0 - K, -K)
@@ -199,7 +202,10 @@ __global__ void __launch_bounds__(32 * kDrWarps) k_row_dr(const KParams p) {
 #pragma unroll
         for (int q = 0; q < NPG; q++) {
           const float2 y = cs[q].step(p, psi[q]);
-          if (c >= x0 && rok) yp[q * yp_pair + (long long)c * p.in_rows] = y;
+          if (c >= x0 && rok) {
+            GC_CHK(p, &yp[q * yp_pair + (long long)c * p.in_rows], 8);
+            yp[q * yp_pair + (long long)c * p.in_rows] = y;
+          }
         }
       }
     }
@@ -236,7 +242,10 @@ __global__ void __launch_bounds__(32 * kDrWarps) k_row_dr(const KParams p) {
   const int nchunk = (x1 - x0 + kDrChunk - 1) / kDrChunk;
   float2 ypn[NPG];
 #pragma unroll
-  for (int q = 0; q < NPG; q++) ypn[q] = yp[q * yp_pair + (long long)(x1 - 1) * p.in_rows];
+  for (int q = 0; q < NPG; q++) {
+    GC_CHK(p, &yp[q * yp_pair + (long long)(x1 - 1) * p.in_rows], 8);
+    ypn[q] = yp[q * yp_pair + (long long)(x1 - 1) * p.in_rows];
+  }
 #pragma unroll 1
   for (int ch = nchunk - 1; ch >= 0; ch--) {
     const int c0 = x0 + ch * kDrChunk, c1 = min(c0 + kDrChunk, x1);
@@ -251,7 +260,10 @@ __global__ void __launch_bounds__(32 * kDrWarps) k_row_dr(const KParams p) {
       for (int q = 0; q < NPG; q++) ypc[q] = ypn[q];
       if (c > x0) {
 #pragma unroll
-        for (int q = 0; q < NPG; q++) ypn[q] = yp[q * yp_pair + (long long)(c - 1) * p.in_rows];
+        for (int q = 0; q < NPG; q++) {
+          GC_CHK(p, &yp[q * yp_pair + (long long)(c - 1) * p.in_rows], 8);
+          ypn[q] = yp[q * yp_pair + (long long)(c - 1) * p.in_rows];
+        }
       }
       float2 psi[NPG];
       dr_planes<NPG>(p, fc[i], psi);
@@ -269,9 +281,15 @@ __global__ void __launch_bounds__(32 * kDrWarps) k_row_dr(const KParams p) {
         const int r = lane / kDrChunk + 4 * i;
         const int rr = rb * 32 + r;
         // (rows r + 16 .. r + 28 are handled by the second half below)
-        if (rr < p.in_rows && c0 + j < c1) dst[q * pstride + (long long)rr * n + c0 + j] = sm.tile[q][r][j];
+        if (rr < p.in_rows && c0 + j < c1) {
+          GC_CHK(p, &dst[q * pstride + (long long)rr * n + c0 + j], 8);
+          dst[q * pstride + (long long)rr * n + c0 + j] = sm.tile[q][r][j];
+        }
         const int r2 = r + 16, rr2 = rb * 32 + r2;
-        if (rr2 < p.in_rows && c0 + j < c1) dst[q * pstride + (long long)rr2 * n + c0 + j] = sm.tile[q][r2][j];
+        if (rr2 < p.in_rows && c0 + j < c1) {
+          GC_CHK(p, &dst[q * pstride + (long long)rr2 * n + c0 + j], 8);
+          dst[q * pstride + (long long)rr2 * n + c0 + j] = sm.tile[q][r2][j];
+        }
       }
     }
     __syncwarp();
@@ -312,7 +330,10 @@ __global__ void __launch_bounds__(32 * kDrWarps) k_col_dr(const KParams p) {
     const int gs = max(g0 - K, -K);
     float2 nx[NPG];
 #pragma unroll
-    for (int q = 0; q < NPG; q++) nx[q] = __ldg(pl + q * pstride + prow(gs));
+    for (int q = 0; q < NPG; q++) {
+      GC_CHK(p, pl + q * pstride + prow(gs), 8);
+      nx[q] = __ldg(pl + q * pstride + prow(gs));
+    }
 #pragma unroll 1
     for (int g = gs; g < g1; g++) {
       float2 cx[NPG];
@@ -321,12 +342,18 @@ __global__ void __launch_bounds__(32 * kDrWarps) k_col_dr(const KParams p) {
       if (g + 1 < g1) {
         const long long o = prow(g + 1);
 #pragma unroll
-        for (int q = 0; q < NPG; q++) nx[q] = __ldg(pl + q * pstride + o);
+        for (int q = 0; q < NPG; q++) {
+          GC_CHK(p, pl + q * pstride + o, 8);
+          nx[q] = __ldg(pl + q * pstride + o);
+        }
       }
 #pragma unroll
       for (int q = 0; q < NPG; q++) {
         const float2 y = cs[q].step(p, cx[q]);
-        if (g >= g0) ys[q * ys_pair + (long long)(g - p.out_row0) * p.Wd] = y;
+        if (g >= g0) {
+          GC_CHK(p, &ys[q * ys_pair + (long long)(g - p.out_row0) * p.Wd], 8);
+          ys[q * ys_pair + (long long)(g - p.out_row0) * p.Wd] = y;
+        }
       }
     }
   }
@@ -343,11 +370,18 @@ __global__ void __launch_bounds__(32 * kDrWarps) k_col_dr(const KParams p) {
   auto fetch = [&](int g) {
     const long long o = prow(g);
 #pragma unroll
-    for (int q = 0; q < NPG; q++) nx[q] = __ldg(pl + q * pstride + o);
+    for (int q = 0; q < NPG; q++) {
+      GC_CHK(p, pl + q * pstride + o, 8);
+      nx[q] = __ldg(pl + q * pstride + o);
+    }
     if (g < g1) {
       const long long oy = (long long)(g - p.out_row0) * p.Wd;
 #pragma unroll
-      for (int q = 0; q < NPG; q++) ny[q] = ys[q * ys_pair + oy];
+      for (int q = 0; q < NPG; q++) {
+        GC_CHK(p, &ys[q * ys_pair + oy], 8);
+        ny[q] = ys[q * ys_pair + oy];
+      }
+      GC_CHK(p, row_ptr(p, b, g) + xc, 4);
       nf = __ldg(row_ptr(p, b, g) + xc);
     }
   };
@@ -394,6 +428,7 @@ __global__ void __launch_bounds__(32 * kDrWarps) k_col_dr(const KParams p) {
         o = fminf(fmaxf(fo, p.L), p.U);
         nguard++;
       }
+      GC_CHK(p, &p.out[b * p.out_img_stride + (long long)yo * p.Wd + x], 4);
       p.out[b * p.out_img_stride + (long long)yo * p.Wd + x] = o;
     }
   }

@@ -83,6 +83,36 @@ __device__ __forceinline__ float ex2_ftz(float x) {
   return y;
 }
 
+// ---- bounds checks of the GC_BOUNDS_CHECK build (libgc_check.so; compute-sanitizer is not
+// available on the B200 pool): [ptr, ptr + bytes) must lie in an input segment (of some image of
+// the batch), the plane / scratch buffer, the output, or the taps; otherwise the access is counted
+// in *p.oob.  GC_CHK compiles to nothing in the product library.
+#ifdef GC_BOUNDS_CHECK
+static __device__ __noinline__ void gc_oob_note(const KParams& p) {
+  if (p.oob) atomicAdd(p.oob, 1ull);
+}
+__device__ __forceinline__ bool gc_in(const void* ptr, size_t n, const void* base, size_t bytes) {
+  const char* a = reinterpret_cast<const char*>(ptr);
+  const char* b = reinterpret_cast<const char*>(base);
+  return base && a >= b && a + n <= b + bytes;
+}
+__device__ __forceinline__ void gc_chk(const KParams& p, const void* ptr, size_t n) {
+  if (gc_in(ptr, n, p.planes, p.planes_bytes)) return;
+  if (gc_in(ptr, n, p.out, (size_t)p.B * p.out_img_stride * 4)) return;
+  if (p.taps_g && gc_in(ptr, n, p.taps_g, (size_t)(2 * p.R + 1) * 16)) return;
+  for (int k = 0; k < 3; k++) {
+    if (p.seg[k].rows <= 0) continue;
+    const size_t img = (size_t)p.seg[k].rows * p.Wd * 4;
+    for (int b = 0; b < p.B; b++)
+      if (gc_in(ptr, n, p.seg[k].ptr + (long long)b * p.seg_img_stride, img)) return;
+  }
+  gc_oob_note(p);
+}
+#define GC_CHK(p, ptr, n) gc_chk((p), (ptr), (n))
+#else
+#define GC_CHK(p, ptr, n) ((void)0)
+#endif
+
 // Pointer to global row gy of image b, found in the input segments.
 __device__ __forceinline__ const float* row_ptr(const KParams& p, int b, int gy) {
 #pragma unroll

@@ -82,4 +82,19 @@ cudaError_t launch_direct(const float* img, int B, int H, int W, int R, float si
   return cudaGetLastError();
 }
 
+// Positive control of the GC_BOUNDS_CHECK machinery (gc_debug_oob_selftest): GC_CHK of one
+// address just past a region and one inside it; only the first may be counted.  No memory is
+// accessed.
+__global__ void k_oob_selftest(const KParams p) {
+  if (threadIdx.x == 0) {
+    GC_CHK(p, reinterpret_cast<const char*>(p.planes) + p.planes_bytes, 1);   // one byte past the end
+    GC_CHK(p, p.planes, 8);                                                      // inside
+  }
+}
+
+cudaError_t launch_oob_selftest(const KParams& p, cudaStream_t s) {
+  k_oob_selftest<<<1, 32, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
 }  // namespace gc

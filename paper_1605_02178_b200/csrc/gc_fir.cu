@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(32 * kRowWarpsPerCta, 16) k_row_t(const KParam
     for (int k = 0; k < C::NLD; k++) {
       const int c = lane + 32 * k;
       const int gx = xint ? x0 - W + c : mirror(x0 - W + c, p.Wd);
+      if (c < C::SW) GC_CHK(p, src + gx, 4);
       fv[rr][k] = (c < C::SW) ? __ldg(src + gx) : 0.f;
     }
   }
@@ -139,10 +140,11 @@ __global__ void __launch_bounds__(32 * kRowWarpsPerCta, 16) k_row_t(const KParam
           const int c = 2 * lane + 64 * h;
           const float2 u = sO[rr * C::OWP + C::pad(c)], v = sO[rr * C::OWP + C::pad(c + 1)];
           if (vec && x0 + c + 1 < p.Wd) {
+            GC_CHK(p, d + c, 16);
             *reinterpret_cast<float4*>(d + c) = make_float4(u.x, u.y, v.x, v.y);
           } else {
-            if (x0 + c < p.Wd) d[c] = u;
-            if (x0 + c + 1 < p.Wd) d[c + 1] = v;
+            if (x0 + c < p.Wd) { GC_CHK(p, d + c, 8); d[c] = u; }
+            if (x0 + c + 1 < p.Wd) { GC_CHK(p, d + c + 1, 8); d[c + 1] = v; }
           }
         }
       }
@@ -299,6 +301,8 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 4)
           if (lane == 0) mbar_arrive(&full[s]);   // sentinel: no more tasks
         } else if (tma_ok && interior) {
           if (lane == 0) {
+            GC_CHK(p, p.planes + ((long long)(b * p.NP + pp) * p.in_rows + (g0 - p.in_row0)) * p.Wd + x0, 8);
+            GC_CHK(p, p.planes + ((long long)(b * p.NP + pp) * p.in_rows + (g0 - p.in_row0) + C::NJ - 1) * p.Wd + x0, 8);
             mbar_expect_tx(&full[s], C::BUFB);
             tma_2d(dst, &tmap, x0, (b * p.NP + pp) * p.in_rows + (g0 - p.in_row0), &full[s]);
           }
@@ -310,6 +314,7 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 4)
           for (int j = lane; j < C::NJ; j += 32) {
             int q = mirror(g0 + min(j, jmax), p.H) - p.in_row0;
             q = min(max(q, 0), p.in_rows - 1);
+            GC_CHK(p, pl + (long long)q * p.Wd, 256);
             bulk_g2s(dst + j * 32, pl + (long long)q * p.Wd, 256, &full[s]);
           }
         } else {
@@ -318,6 +323,7 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 4)
           for (int j = 0; j < C::NJ; j++) {
             int q = mirror(g0 + min(j, jmax), p.H) - p.in_row0;
             q = min(max(q, 0), p.in_rows - 1);
+            if (x0 + lane < p.Wd) GC_CHK(p, pl + (long long)q * p.Wd + lane, 8);
             dst[j * 32 + lane] = (x0 + lane < p.Wd) ? pl[(long long)q * p.Wd + lane] : make_float2(0.f, 0.f);
           }
           __syncwarp();
@@ -351,11 +357,15 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 4)
       const float* run = ya + RY - 1 <= last ? row_run_ptr(p, b, p.out_row0 + ya, RY) : nullptr;
       if (run) {
 #pragma unroll
-        for (int i = 0; i < RY; i++) fo[i] = (x < p.Wd) ? __ldg(run + (long long)i * p.Wd + x) : 0.f;
+        for (int i = 0; i < RY; i++) {
+          if (x < p.Wd) GC_CHK(p, run + (long long)i * p.Wd + x, 4);
+          fo[i] = (x < p.Wd) ? __ldg(run + (long long)i * p.Wd + x) : 0.f;
+        }
       } else {
 #pragma unroll
         for (int i = 0; i < RY; i++) {
           const int yy = min(ya + i, last);
+          if (x < p.Wd) GC_CHK(p, row_ptr(p, b, p.out_row0 + yy) + x, 4);
           fo[i] = (x < p.Wd) ? __ldg(row_ptr(p, b, p.out_row0 + yy) + x) : 0.f;
         }
       }
@@ -417,6 +427,7 @@ __global__ void __launch_bounds__(32 * (kColConsumers + 1), 4)
           o = fminf(fmaxf(fo[i], p.L), p.U);
           nguard++;
         }
+        GC_CHK(p, &out[(long long)yy * p.Wd], 4);
         out[(long long)yy * p.Wd] = o;
       }
     }
@@ -443,6 +454,7 @@ __global__ void __launch_bounds__(256) k_row_rt(const KParams p) {
     const float* src = row_ptr(p, b, p.in_row0 + rr);
     for (int c = tid; c < SW; c += 256) {
       float a, e;
+      GC_CHK(p, src + mirror(x0 - R + c, p.Wd), 4);
       const float fv = __ldg(src + mirror(x0 - R + c, p.Wd));
       centre(p, fv, a, e);
       if (p.raw) { e = fv; a = 0.f; }
@@ -459,6 +471,7 @@ __global__ void __launch_bounds__(256) k_row_rt(const KParams p) {
     if (ok) {
       float2 acc = make_float2(0.f, 0.f);
       for (int m = 0; m <= 2 * R; m++) acc = f2fma(p.taps_g[m], sPL[r * SW + xo + m], acc);
+      GC_CHK(p, &p.planes[b * p.planes_img_stride + pp * pstride + (long long)rr * p.Wd + x0 + xo], 8);
       p.planes[b * p.planes_img_stride + pp * pstride + (long long)rr * p.Wd + x0 + xo] = acc;
     }
     __syncthreads();
@@ -477,6 +490,7 @@ __global__ void __launch_bounds__(256) k_col_rt(const KParams p) {
   const int R = p.R;
   const int gy = p.out_row0 + y;
   float a, e;
+  GC_CHK(p, row_ptr(p, b, gy) + x, 4);
   const float f = __ldg(row_ptr(p, b, gy) + x);
   centre(p, f, a, e);
   const float a2 = a * a;
@@ -488,6 +502,7 @@ __global__ void __launch_bounds__(256) k_col_rt(const KParams p) {
     float2 acc = make_float2(0.f, 0.f);
     for (int m = 0; m <= 2 * R; m++) {
       const int q = mirror(gy + m - R, p.H) - p.in_row0;
+      GC_CHK(p, pl + (long long)q * p.Wd, 8);
       acc = f2fma(p.taps_g[m], __ldg(pl + (long long)q * p.Wd), acc);
     }
     if (pp == 0) raw0 = acc.x;
@@ -509,6 +524,7 @@ __global__ void __launch_bounds__(256) k_col_rt(const KParams p) {
     guarded = 1;
   }
   count_guarded(p.fallback, __activemask(), guarded);
+  GC_CHK(p, &p.out[b * p.out_img_stride + (long long)y * p.Wd + x], 4);
   p.out[b * p.out_img_stride + (long long)y * p.Wd + x] = o;
 }
 

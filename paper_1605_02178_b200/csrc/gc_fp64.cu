@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(256) k_row_f64(const KParams p) {
     const float* src = row_ptr(p, b, p.in_row0 + rr);
     for (int c = tid; c < SW; c += 256) {
       double a, e;
+      GC_CHK(p, src + mirror(x0 - R + c, p.Wd), 4);
       centre_d(p, __ldg(src + mirror(x0 - R + c, p.Wd)), a, e);
       sPL[r * SW + c] = make_double2(e, e * a);
       sA2[r * SW + c] = a * a;
@@ -59,6 +60,7 @@ __global__ void __launch_bounds__(256) k_row_f64(const KParams p) {
         ax = fma(k, v.x, ax);
         ay = fma(k, v.y, ay);
       }
+      GC_CHK(p, &planes[b * p.planes_img_stride + pp * pstride + (long long)rr * p.Wd + x0 + xo], 16);
       planes[b * p.planes_img_stride + pp * pstride + (long long)rr * p.Wd + x0 + xo] = make_double2(ax, ay);
     }
     __syncthreads();
@@ -81,6 +83,7 @@ __global__ void __launch_bounds__(256) k_col_f64(const KParams p) {
   if (live) {
     const int R = p.R;
     const int gy = p.out_row0 + y;
+    GC_CHK(p, row_ptr(p, b, gy) + x, 4);
     const float f = __ldg(row_ptr(p, b, gy) + x);
     double a, e;
     centre_d(p, f, a, e);
@@ -92,6 +95,7 @@ __global__ void __launch_bounds__(256) k_col_f64(const KParams p) {
       double fx = 0.0, fy = 0.0;                          // (Fbar'_{2p}, Fbar'_{2p+1})
       for (int m = 0; m <= 2 * R; m++) {
         const int q = mirror(gy + m - R, p.H) - p.in_row0;
+        GC_CHK(p, &pl[(long long)q * p.Wd], 16);
         const double2 v = pl[(long long)q * p.Wd];
         fx = fma(p.taps_d[m], v.x, fx);
         fy = fma(p.taps_d[m], v.y, fy);
@@ -113,6 +117,7 @@ __global__ void __launch_bounds__(256) k_col_f64(const KParams p) {
       o = (float)fmin(fmax((double)f, p.d_L), p.d_U);
       guarded = 1;
     }
+    GC_CHK(p, &p.out[b * p.out_img_stride + (long long)y * p.Wd + x], 4);
     p.out[b * p.out_img_stride + (long long)y * p.Wd + x] = o;
   }
   count_guarded(p.fallback, __activemask(), guarded);

@@ -20,6 +20,8 @@ gc_status coeffs_cached(int N, double sigma_r, double L, double U, std::vector<d
 
 // Stream-ordered scratch from libgc's private per-device pool (gc_api.cpp); free with cudaFreeAsync.
 cudaError_t scratch_alloc(void** ptr, size_t bytes, cudaStream_t s);
+// GC_BOUNDS_CHECK builds: device counter of out-of-bounds accesses (nullptr otherwise).
+unsigned long long* oob_counter();
 
 constexpr int kMaxPlanes = GC_N_MAX + 2 + 1;   // N+2 planes, rounded up to even
 constexpr int kMaxPairs = (kMaxPlanes + 1) / 2;
@@ -59,6 +61,10 @@ struct KParams {
   float inv_th;           // 1/t_h   (a' = g / t_h in [-1, 1])
   float ex_k;             // -mu/2 * log2(e):  exp(-g^2/2sr^2) = exp2(ex_k a'^2)
   unsigned long long* fallback;  // may be null
+  // GC_BOUNDS_CHECK builds (libgc_check.so): every global access of the kernels is checked against
+  // the buffers below and violations are counted in *oob (gc_debug_oob_count); null otherwise
+  unsigned long long* oob;
+  size_t planes_bytes;    // bytes of the plane buffer (incl. counters and the Deriche scratch)
   const float2* taps_g;   // (k_m, k_m), m = 0..2R, in global memory (runtime-W kernels)
   cudaEvent_t ev[3];      // optional timing events (host side only; not read on device)
   float2 chat2[kMaxPairs];         // (chat_{2p}, chat_{2p+1}), zero beyond N
@@ -180,6 +186,9 @@ cudaError_t launch_deriche_two_pass(const KParams& p, cudaStream_t stream);
 
 // Two-pass FIR pipeline in binary64 (gc_fp64.cu): planes are double2 pairs (twice the bytes).
 cudaError_t launch_fp64_two_pass(const KParams& p, cudaStream_t stream);
+
+// GC_BOUNDS_CHECK positive control (gc_direct.cu): counts exactly one out-of-bounds access.
+cudaError_t launch_oob_selftest(const KParams& p, cudaStream_t s);
 
 // Direct bilateral filter of eq. (1) (gc_direct.cu).
 cudaError_t launch_direct(const float* img, int B, int H, int W, int R, float sigma_s, float sigma_r, float* out,

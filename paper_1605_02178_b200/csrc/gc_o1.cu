@@ -35,6 +35,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -68,12 +69,18 @@ __device__ __forceinline__ void o1_prefetch_row(const KParams& p, float* raw, co
   if (vec && pc >= 0 && pc + kO1CH <= p.Wd) {
 #pragma unroll
     for (int k = 0; k < kO1CH / 4; k++)
+    {
+      GC_CHK(p, rowp + pc + 4 * k, 16);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s + 16 * k), "l"(rowp + pc + 4 * k) : "memory");
+    }
   } else {
 #pragma unroll 1
     for (int k = 0; k < kO1CH; k++)
+    {
+      GC_CHK(p, rowp + mirror(pc + k, p.Wd), 4);
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s + 4 * k), "l"(rowp + mirror(pc + k, p.Wd))
                    : "memory");
+    }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -83,7 +90,14 @@ __device__ __forceinline__ void o1_prefetch_row(const KParams& p, float* raw, co
 // gc_gaussian; then F'_{2p0+1} = v.x v.y and the pair step is a'^2 = v.y^2.
 // (f comes from the prefetch buffer `raw`, whose cp.async group the caller has waited for; the
 // next chunk of the same stream is prefetched into it afterwards)
-template <int WAIT>
+// (inlined: as a call, the ABI saves the caller's ~100 live state registers around it — measured
+// 8.2 instead of 6.0 ms for the c5 row pass)
+// PM = plane-generation mode, a template parameter so that each row-pass instantiation carries one
+// staging variant (four inlined sites per task; ncu r02: no_instruction stalls): 0 = gc_gaussian
+// (f, 0), 1 = first pair group (p0 = 0), 2 = p0 = 4, 3 = any p0.
+enum { kPmRaw = 0, kPm0 = 1, kPm4 = 2, kPmAny = 3 };
+
+template <int WAIT, int PM>
 __device__ __forceinline__ void o1_stage_row(const KParams& p, float2* t, float* raw, const float* rowp, int pc,
                                             int lane, bool vec, int p0) {
   asm volatile("cp.async.wait_group %0;" ::"n"(WAIT) : "memory");
@@ -98,17 +112,17 @@ __device__ __forceinline__ void o1_stage_row(const KParams& p, float2* t, float*
   }
   float2* d = t + lane * kO1TS;
   __syncwarp();
-  if (p.raw) {
+  if constexpr (PM == kPmRaw) {
 #pragma unroll
     for (int k = 0; k < kO1CH; k++) d[k] = make_float2(v[k], 0.f);
-  } else if (p0 == 0) {
+  } else if constexpr (PM == kPm0) {
 #pragma unroll
     for (int k = 0; k < kO1CH; k++) {
       float a, e;
       centre(p, v[k], a, e);
       d[k] = make_float2(e, a);
     }
-  } else if (p0 == 4) {
+  } else if constexpr (PM == kPm4) {
 #pragma unroll
     for (int k = 0; k < kO1CH; k++) {
       float a, e;
@@ -164,15 +178,15 @@ struct RowO1State {
 };
 
 // One output step at x (window centred on x), output slot j of the current store chunk.
-template <int NPG>
+template <int NPG, int PM>
 __device__ __forceinline__ void row_o1_step(const KParams& p, RowO1Smem& sm, RowO1State<NPG>& st, int x, int j,
                                             const float* rowp, bool vec, int p0, int lane) {
   const int R = p.R;
   const int pe_pos = x + R + 1, pl_pos = x - R;
   // the two streams stage on different steps ((2W+1) is odd), so the newest cp.async group is
   // always the other stream's prefetch: wait_group 1 finds this stream's chunk complete
-  if ((pe_pos & (kO1CH - 1)) == 0) o1_stage_row<1>(p, sm.fin, sm.raw[0], rowp, pe_pos, lane, vec, p0);
-  if ((pl_pos & (kO1CH - 1)) == 0) o1_stage_row<1>(p, sm.fout, sm.raw[1], rowp, pl_pos, lane, vec, p0);
+  if ((pe_pos & (kO1CH - 1)) == 0) o1_stage_row<1, PM>(p, sm.fin, sm.raw[0], rowp, pe_pos, lane, vec, p0);
+  if ((pl_pos & (kO1CH - 1)) == 0) o1_stage_row<1, PM>(p, sm.fout, sm.raw[1], rowp, pl_pos, lane, vec, p0);
   const float2 ve = sm.fin[lane * kO1TS + (pe_pos & (kO1CH - 1))];
   const float2 vl = sm.fout[lane * kO1TS + (pl_pos & (kO1CH - 1))];
   float2 pe = make_float2(ve.x, ve.x * ve.y), pl = make_float2(vl.x, vl.x * vl.y);
@@ -188,7 +202,7 @@ __device__ __forceinline__ void row_o1_step(const KParams& p, RowO1Smem& sm, Row
   }
 }
 
-template <int NPG>
+template <int NPG, int PM>
 __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int b, int r0, int xs, int xe, int p0,
                                             int lane) {
   const int R = p.R;
@@ -211,7 +225,7 @@ __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int
   for (int s = 0; s < lead; s++) {
     const int pos = P0 + s;
     if (s == 0 || (pos & (kO1CH - 1)) == 0)      // (only this stream stages here: wait for all groups)
-      o1_stage_row<0>(p, sm.fin, sm.raw[0], rowp, pos & ~(kO1CH - 1), lane, vec, p0);
+      o1_stage_row<0, PM>(p, sm.fin, sm.raw[0], rowp, pos & ~(kO1CH - 1), lane, vec, p0);
     const float2 ve = sm.fin[lane * kO1TS + (pos & (kO1CH - 1))];
     float2 pe = make_float2(ve.x, ve.x * ve.y);
     const float a2e = ve.y * ve.y;
@@ -225,7 +239,7 @@ __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int
   // ---- outputs x = xs .. xe-1, in chunks of kO1OC positions (xs is a multiple of 32).  The
   // leaving stream's first chunk: staged here unless x = xs itself starts a chunk (then the first
   // step stages it; staging it twice would read the prefetch of the chunk after it)
-  if ((xs - R) & (kO1CH - 1)) o1_stage_row<0>(p, sm.fout, sm.raw[1], rowp, (xs - R) & ~(kO1CH - 1), lane, vec, p0);
+  if ((xs - R) & (kO1CH - 1)) o1_stage_row<0, PM>(p, sm.fout, sm.raw[1], rowp, (xs - R) & ~(kO1CH - 1), lane, vec, p0);
   // O(1) plane layout [B][rows][NP][Wd]: the NP pairs of one image row are adjacent rows of
   // a 2-D [B*rows*NP][Wd] tensor, so the column pass fetches a row's pairs with one TMA box
   const long long rstride = (long long)p.NP * p.Wd;         // float2 between image rows
@@ -238,7 +252,7 @@ __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int
   for (int x = xs; x < xe; x += kO1OC) {
     const int nb = min(kO1OC, xe - x);
 #pragma unroll 1
-    for (int j = 0; j < nb; j++) row_o1_step<NPG>(p, sm, st, x + j, j, rowp, vec, p0, lane);
+    for (int j = 0; j < nb; j++) row_o1_step<NPG, PM>(p, sm, st, x + j, j, rowp, vec, p0, lane);
     // store the chunk: per pair, kO1OC positions x 32 rows (ORS rows x 8 kO1OC bytes per instruction)
     __syncwarp();
     if (ocol < nb) {
@@ -247,7 +261,10 @@ __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int
       for (int q = 0; q < NPG; q++) {
 #pragma unroll
         for (int j = 0; j < 32 / ORS; j++)
-          if (ORS * j < rows_left) o[(long long)(ORS * j) * rstride] = sm.o[q][ocol][ORS * j + orow];
+          if (ORS * j < rows_left) {
+            GC_CHK(p, &o[(long long)(ORS * j) * rstride], 8);
+            o[(long long)(ORS * j) * rstride] = sm.o[q][ocol][ORS * j + orow];
+          }
         o += p.Wd;
       }
     }
@@ -275,12 +292,22 @@ __global__ void __launch_bounds__(32 * kO1Warps, 3) k_row_o1(const KParams p) {
   const int xs = sx * p.o1_seg_x, xe = min(xs + p.o1_seg_x, p.Wd);
   const int p0 = g * kO1RowNPG;
   const int npl = min(kO1RowNPG, p.NP - p0);
-  switch (npl) {
-    case 1: row_o1_task<1>(p, sm, b, rb * 32, xs, xe, p0, lane); break;
-    case 2: row_o1_task<2>(p, sm, b, rb * 32, xs, xe, p0, lane); break;
-    case 3: row_o1_task<3>(p, sm, b, rb * 32, xs, xe, p0, lane); break;
-    default: row_o1_task<4>(p, sm, b, rb * 32, xs, xe, p0, lane); break;
+  if (p.raw) {                                   // gc_gaussian: one pair (f, 0)
+    row_o1_task<1, kPmRaw>(p, sm, b, rb * 32, xs, xe, p0, lane);
+    return;
   }
+  auto go = [&](auto pm) {
+    constexpr int PM = decltype(pm)::value;
+    switch (npl) {
+      case 1: row_o1_task<1, PM>(p, sm, b, rb * 32, xs, xe, p0, lane); break;
+      case 2: row_o1_task<2, PM>(p, sm, b, rb * 32, xs, xe, p0, lane); break;
+      case 3: row_o1_task<3, PM>(p, sm, b, rb * 32, xs, xe, p0, lane); break;
+      default: row_o1_task<4, PM>(p, sm, b, rb * 32, xs, xe, p0, lane); break;
+    }
+  };
+  if (p0 == 0) go(std::integral_constant<int, kPm0>());
+  else if (p0 == 4) go(std::integral_constant<int, kPm4>());
+  else go(std::integral_constant<int, kPmAny>());
 }
 
 // ------------------------------------------------------------------ column pass + eqs. (8)-(10)
@@ -415,12 +442,15 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const __grid_constant_
 #pragma unroll
       for (int q = 0; q < NPG; q++) {
         if (q < npl) {
+          GC_CHK(p, src + q * p.Wd + re, 8);
+          GC_CHK(p, src + q * p.Wd + rl, 8);
           cp_async8(&sm.ring[st][0][q][lane], src + q * p.Wd + re);
           cp_async8(&sm.ring[st][1][q][lane], src + q * p.Wd + rl);
         }
       }
     }
     const int fi = max(i, 0);
+    GC_CHK(p, fseg ? frow + (long long)fi * p.Wd : row_ptr(p, b, p.out_row0 + fi) + xc, 4);
     cp_async4(&sm.fring[st][lane], fseg ? frow + (long long)fi * p.Wd : row_ptr(p, b, p.out_row0 + fi) + xc);
   };
   const int i0 = ys - lead;
@@ -494,6 +524,7 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const __grid_constant_
           o = fminf(fmaxf(fo, p.L), p.U);
           nguard++;
         }
+        GC_CHK(p, &outp[(long long)i * p.Wd], 4);
         outp[(long long)i * p.Wd] = o;
       }
     }
@@ -527,7 +558,6 @@ __global__ void __launch_bounds__(32 * kO1Warps) k_col_o1(const __grid_constant_
 constexpr int kPDMax = 48;       // ring stages (at most)
 constexpr int kRPS = 4;          // image rows per ring stage: one [4 NP x 32] TMA box per direction in the
                                  // interior (per-row boxes where the rows are mirrored or clamped)
-constexpr int kPRB = 8;          // output rows per fold block (two ring stages: static ring offsets)
 
 // Shared memory: this head, then the ring of nst stages, each = kRPS entering rows followed by
 // kRPS leaving rows, a row = [NP pairs x 32 columns] float2.
@@ -535,7 +565,7 @@ template <int NP>
 struct alignas(1024) ColPSmem {
   unsigned long long full[kPDMax], empty[kPDMax];
   unsigned long long tile_full[2], tile_free[2];   // per tile buffer: all NP warps wrote / folded it
-  float2 tile[2][kPRB][NP][32];  // [buffer][row in block][pair][column]
+  float2 tile[2][NP][NP][32];    // [buffer][row in block][pair][column]; a fold block = NP rows
 };
 template <int NP>
 __host__ __device__ constexpr size_t colp_head() { return (sizeof(ColPSmem<NP>) + 1023) / 1024 * 1024; }
@@ -565,6 +595,22 @@ __device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned phase) {
       "}\n" ::"r"(bar),
       "r"(phase)
       : "memory");
+}
+__device__ __forceinline__ void mbar_wait_backoff(unsigned bar, unsigned phase) {
+  for (;;) {
+    unsigned ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(phase)
+        : "memory");
+    if (ok) return;
+    __nanosleep(128);
+  }
 }
 __device__ __forceinline__ float2 lds64(unsigned a) {
   float2 v;
@@ -638,11 +684,15 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
       auto load = [&](unsigned dst, int g0, unsigned bar, unsigned long long pol) {
         const int r0 = g0 - p.in_row0;
         if (g0 >= 0 && g0 + kRPS <= p.H && r0 >= 0 && r0 + kRPS <= p.in_rows) {
+          GC_CHK(p, p.planes + ((long long)(ybase + r0) * NP) * p.Wd + x0, 8);                  // first and last
+          GC_CHK(p, p.planes + ((long long)(ybase + r0 + kRPS) * NP - 1) * p.Wd + x0, 8);       // row of the box
           tma_2d_hint(dst, &tmap4, x0, (ybase + r0) * NP, bar, pol);            // interior: one box
         } else {
 #pragma unroll 1
           for (int r = 0; r < kRPS; r++) {                                    // mirrored / clamped rows
             const int rr = min(max(mirror(g0 + r, p.H) - p.in_row0, 0), p.in_rows - 1);
+            GC_CHK(p, p.planes + ((long long)(ybase + rr) * NP) * p.Wd + x0, 8);
+            GC_CHK(p, p.planes + ((long long)(ybase + rr + 1) * NP - 1) * p.Wd + x0, 8);
             tma_2d_hint(dst + r * BOX, &tmap, x0, (ybase + rr) * NP, bar, pol);
           }
         }
@@ -650,7 +700,9 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
       int st = 0;
       unsigned ph = 0;
       for (int g = 0; g < ngroups; g++) {
-        if (g >= nst) mbar_wait_u32(smem_u32(&sm.empty[st]), ph ^ 1);
+        // (the ring is full most of the time: back off instead of spinning on the consumers'
+        // issue slots)
+        if (g >= nst) mbar_wait_backoff(smem_u32(&sm.empty[st]), ph ^ 1);
         const int k0 = g * kRPS;                    // first step of the group
         const bool leave = k0 + kRPS - 1 >= zl;     // some step of the group has a real leaving row
         const unsigned bar = smem_u32(&sm.full[st]);
@@ -710,65 +762,57 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
   float* const outp = p.out + b * p.out_img_stride + x;
   unsigned nguard = 0;
   const unsigned tf0 = smem_u32(&sm.tile_full[0]), tr0 = smem_u32(&sm.tile_free[0]);
-  // Blocks of kPRB output rows.  Block blk is filtered into tile buffer blk & 1 while block blk-1 is
-  // folded (eqs. 8-10) from the other buffer: warp q folds rows r = (q - blk') mod NP, + NP, ...
-  // (rotated per block, so the kPRB - NP extra rows spread over the warps), and the mbarriers
-  // tile_full / tile_free give every warp a block of slack instead of a per-block barrier.
-  const int nblk = (ye - ys + kPRB - 1) / kPRB;
-  float fo = 0.f, fo2 = 0.f;                        // f at the first two rows this warp folds next
+  // Blocks of NP output rows: block blk is filtered into tile buffer blk & 1 while block blk-1 is
+  // folded (eqs. 8-10) from the other buffer, warp q folding row q — every warp does the same work
+  // per block.  The mbarriers tile_full / tile_free give each warp a block of slack.  (Ring stages
+  // hold kRPS rows, so the stage position r is a runtime counter here.)
+  const int nblk = (ye - ys + NP - 1) / NP;
+  int r = 0;                                        // row within the current ring stage
+  float fo = 0.f;                                   // f at the row this warp folds next
 #pragma unroll 1
   for (int blk = 0; blk <= nblk; blk++) {
-    const int bs = ys + blk * kPRB;
+    const int bs = ys + blk * NP;
     const int pb = blk - 1;                         // block folded in this iteration
-    const int pbs = bs - kPRB;
-    const int pnb = pb >= 0 ? min(kPRB, ye - pbs) : 0;
-    const int r0 = pb >= 0 ? (q - pb % NP + NP) % NP : 0;
-    if (pb >= 0) {                                  // f for the fold below, loaded before the filtering
-      fo = r0 < pnb ? __ldg(row_ptr(p, b, p.out_row0 + pbs + r0) + xc) : 0.f;
-      fo2 = r0 + NP < pnb ? __ldg(row_ptr(p, b, p.out_row0 + pbs + r0 + NP) + xc) : 0.f;
+    const int pbs = bs - NP;
+    const int pnb = pb >= 0 ? min(NP, ye - pbs) : 0;
+    if (pb >= 0 && q < pnb) {                       // used after the filtering
+      GC_CHK(p, row_ptr(p, b, p.out_row0 + pbs + q) + xc, 4);
+      fo = __ldg(row_ptr(p, b, p.out_row0 + pbs + q) + xc);
     }
     if (blk < nblk) {                               // ---- filter block blk into tile buffer blk & 1
       const unsigned buf = blk & 1;
-      const int nb = min(kPRB, ye - bs);
+      const int nb = min(NP, ye - bs);
       if (blk >= 2) mbar_wait_u32(tr0 + 8 * buf, ((blk >> 1) - 1) & 1);   // block blk-2 folded
-      float2* const tb = my_tile + buf * (kPRB * BOXF);
-      if (nb == kPRB) {
-#pragma unroll
-        for (int h = 0; h < kPRB / kRPS; h++) {
-          acquire();
-#pragma unroll
-          for (int r = 0; r < kRPS; r++) {
-            const float2 pe = sbase[r * BOXF], pl = sbase[DIRF + r * BOXF];
-            tb[(h * kRPS + r) * BOXF] = o1_output(p, S0, S);   // filtered pair q, row bs + h kRPS + r
-            advance(pe, pl);
-          }
+      float2* const tb = my_tile + buf * (NP * BOXF);
+      auto step = [&](int jj) {
+        if (r == 0) acquire();
+        const float2 pe = sbase[r * BOXF], pl = sbase[DIRF + r * BOXF];
+        tb[jj * BOXF] = o1_output(p, S0, S);        // filtered pair q at row bs + jj
+        advance(pe, pl);
+        if (++r == kRPS) {
           release();
+          r = 0;
         }
+      };
+      if (nb == NP) {
+#pragma unroll
+        for (int jj = 0; jj < NP; jj++) step(jj);
       } else {
 #pragma unroll 1
-        for (int jj = 0; jj < nb; jj++) {
-          const int r = jj % kRPS;
-          if (r == 0) acquire();
-          const float2 pe = sbase[r * BOXF], pl = sbase[DIRF + r * BOXF];
-          tb[jj * BOXF] = o1_output(p, S0, S);
-          advance(pe, pl);
-          if (r == kRPS - 1 || jj == nb - 1) release();
-        }
+        for (int jj = 0; jj < nb; jj++) step(jj);
       }
       __syncwarp();
       if (lane == 0) o1_mbar_arrive(&sm.tile_full[buf]);
     }
-    if (pb >= 0) {                                  // ---- fold block pb: eqs. (8)-(10)
+    if (pb >= 0) {                                  // ---- fold row q of block pb: eqs. (8)-(10)
       const unsigned pbuf = pb & 1;
       mbar_wait_u32(tf0 + 8 * pbuf, (pb >> 1) & 1);   // every warp's pair of block pb is in
-#pragma unroll 1
-      for (int row = r0, t = 0; row < pnb; row += NP, t++) {
-        const float f0 = t == 0 ? fo : t == 1 ? fo2 : __ldg(row_ptr(p, b, p.out_row0 + pbs + row) + xc);
-        const float a = p.raw ? 0.f : centre_a(p, f0);
+      if (q < pnb) {
+        const float a = p.raw ? 0.f : centre_a(p, fo);
         const float a2 = a * a;
         float2 Q2 = make_float2(0.f, 0.f), P2 = Q2, pw2 = make_float2(1.f, a);
         float vprev = 0.f, out_raw = 0.f;
-        const float2* const rt = &sm.tile[pbuf][row][0][lane];
+        const float2* const rt = &sm.tile[pbuf][q][0][lane];
 #pragma unroll
         for (int qq = 0; qq < NP; qq++) {
           const float2 y = rt[qq * 32];
@@ -787,10 +831,11 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
           } else if (Q > 0.f && isfinite(Q) && isfinite(P)) {
             o = p.t_c + p.t_h * __fdividef(P, Q);          // eq. (10) + uncentring
           } else {                                         // guard (R8)
-            o = fminf(fmaxf(f0, p.L), p.U);
+            o = fminf(fmaxf(fo, p.L), p.U);
             nguard++;
           }
-          outp[(long long)(pbs + row) * p.Wd] = o;
+          GC_CHK(p, &outp[(long long)(pbs + q) * p.Wd], 4);
+          outp[(long long)(pbs + q) * p.Wd] = o;
         }
       }
       __syncwarp();
@@ -884,7 +929,7 @@ cudaError_t launch_colp(const KParams& p0, cudaStream_t s) {
   const size_t cap = std::min<size_t>((size_t)(smem_sm > 0 ? smem_sm : 233472) / ctas - 1024, 227 * 1024);
   int nst = (int)((cap - colp_head<NP>()) / colp_stage<NP>());
   if (const char* env = std::getenv("GC_O1P_STAGES")) nst = std::min(nst, std::atoi(env));
-  nst = std::max(kPRB / kRPS, std::min(nst, kPDMax));   // (>= one fold block: no producer starvation)
+  nst = std::max((NP + kRPS - 1) / kRPS + 1, std::min(nst, kPDMax));   // (> one fold block: no starvation)
   const size_t smem = colp_head<NP>() + (size_t)nst * colp_stage<NP>();
   static std::atomic<unsigned long long> ready{0};   // opt in to the largest ring once per device
   const cudaError_t e = once_per_device(ready, [&]() {

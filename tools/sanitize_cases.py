@@ -1,8 +1,12 @@
-"""Small invocations of every libgc device path, for compute-sanitizer (memcheck / racecheck /
-synccheck / initcheck).  Development tool: exits 0 when every call returned GC_OK and the
-outputs are finite; correctness is the tests' job.
+"""Small invocations of every libgc device path, run against the bounds-checked library
+(compute-sanitizer is not available on the B200 pool):
 
-    compute-sanitizer --tool memcheck python tools/sanitize_cases.py
+    GC_LIB_PATH=paper_1605_02178_b200/libgc_check.so python tools/sanitize_cases.py
+
+Every global-memory access of the kernels is range-checked in that build (gc_device.cuh GC_CHK);
+this prints the number of out-of-bounds accesses the cases made and exits non-zero if any (or if
+a call failed or an output is non-finite).  Output buffers also carry NaN guard margins that must
+be untouched.  tests/test_gpu_bounds.py runs it.
 """
 import os
 import sys
@@ -26,6 +30,7 @@ def dev(a):
 def main():
     torch.cuda.set_device(0)
     outs = []
+    checked = "bounds-check" in gc.version()
     # whole images: the three operators, even and odd widths (TMA vs cp.async O(1) column paths)
     for (H, W) in [(64, 96), (61, 77), (1, 33), (40, 1)]:
         x = dev(config_image("c2", H=max(H, 2), W=max(W, 2))[:H, :W])
@@ -62,10 +67,24 @@ def main():
     h = np.ascontiguousarray(config_image("c2", H=300, W=128))
     for op in (OP_FIR, OP_O1, OP_DR):
         outs.append(torch.from_numpy(gc.filter_host(h, 5.0, 70.0, 8, op=op)))
+    # guard margins around caller outputs: libgc must write exactly the H x W block
+    for op, s in ((OP_FIR, 3.0), (OP_O1, 9.0), (OP_O1, 16.0), (OP_DR, 3.0)):
+        x = dev(config_image("c5", H=130, W=98))
+        oc = gc.filter(x, s, 55.0, 12, op=op)
+        flat = torch.full((130 * 98 + 2 * 4096,), float("nan"), device="cuda")
+        mid = flat[4096:4096 + 130 * 98].view(130, 98)            # contiguous block with margins
+        gc.filter(x, s, 55.0, 12, op=op, out=mid)
+        torch.cuda.synchronize()
+        guard_ok = bool(torch.isnan(flat[:4096]).all() and torch.isnan(flat[4096 + 130 * 98:]).all())
+        if not guard_ok or not torch.equal(mid, oc):
+            print(f"sanitize_cases: guard margin written or result differs (op {op}, sigma_s {s})")
+            return 1
     torch.cuda.synchronize()
     bad = [i for i, o in enumerate(outs) if not torch.isfinite(o).all()]
-    print(f"sanitize_cases: {len(outs)} calls, non-finite outputs: {bad}")
-    return 1 if bad else 0
+    oob = gc.debug_oob_count() if checked else None
+    print(f"sanitize_cases: {len(outs)} calls ({gc.version()}), non-finite outputs: {bad}, "
+          f"out-of-bounds accesses: {oob}")
+    return 1 if bad or (oob or 0) > 0 else 0
 
 
 if __name__ == "__main__":

@@ -117,8 +117,8 @@ def alg_instr(N):
     return {"k_row": total - col, "k_col": col, "total": total}
 
 
-O1_FLOP_PER_PLANE = 50   # exact-window recursion per plane-sample and pass:
-#                          A, B (2 add) + box (2 add, 1 mul) + 5 resonators x (3 FMA + 1 add + 1 FMA)
+O1_FLOP_PER_PLANE = 37   # exact-window recursion per plane-sample and pass: A, B (2 add) +
+#                          box (1 sub + 1 FMA) + 4 resonators x (3 FMA + 1 add) + output (4 add)
 DR_FLOP_PER_PLANE = 35   # Deriche mode per plane-sample and pass: 2 sections x 4 FMA per direction
 #                          (16 FMA = 32 FLOP) + 3 adds (section sums, causal + anticausal)
 
@@ -129,7 +129,7 @@ def resolve_op(op, R):
 
 
 def op_flop_per_plane(op, R):
-    """FLOP of the implemented spatial operator per plane-pixel and pass: FIR 2(2R+1); O(1) 50;
+    """FLOP of the implemented spatial operator per plane-pixel and pass: FIR 2(2R+1); O(1) 37;
     Deriche 35 (lead-in samples excluded)."""
     return {1: 2 * (2 * R + 1), 2: O1_FLOP_PER_PLANE, 3: DR_FLOP_PER_PLANE}[op]
 
@@ -171,7 +171,7 @@ def roofline(N, R, op, px, row_ms, col_ms, step_ms, traffic_key=None):
            "step_frac": alg["total"] * px / (step_ms / 1e3) / 1e12 / FP32_PEAK_TINSTR,
            "design": {"achieved": design, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                       "frac": design / FP32_PEAK_TFLOPS,
-                      "basis": "implemented FLOP: " + {1: "FIR 2(2W+1)", 2: "O(1) 50", 3: "Deriche 35"}[op] +
+                      "basis": "implemented FLOP: " + {1: "FIR 2(2W+1)", 2: "O(1) 37", 3: "Deriche 35"}[op] +
                                " per plane-pixel and pass + generation / recombination"},
            "traffic": None}
     tp = os.path.join(ROOT, "profiles", "traffic.json")

@@ -64,8 +64,9 @@ typedef enum {
   GC_OP_AUTO = 0,  /* library choice by W_s: FIR for W_s <= 24, O1 above  */
   GC_OP_FIR = 1,   /* direct separable FIR, 2(2W_s+1) FMA per plane-pixel; W_s <= 1024   */
   GC_OP_O1 = 2,    /* exact-window O(1) recursion: the truncated window of eq. (7) with
-                      the taps replaced by a 6-term cosine least-squares fit (max error
-                      ~1e-6 of the peak tap); 30 FMA-class ops per plane-pixel and pass,
+                      the taps replaced by a 5-term cosine fit with optimised frequencies
+                      (max error ~5e-8 of the peak tap); 24 packed FP32x2 ops per plane-pixel
+                      pair and pass,
                       independent of sigma_s; W_s <= 4096                                  */
   GC_OP_DERICHE = 3 /* NOT eq. (7): the untruncated 4th-order recursive Gaussian of
                       [Deriche1993] that P:50 / P:112 cite for the O(1) claim (SURVEY §8(f)

@@ -27,7 +27,7 @@ constexpr int kMaxPlanes = GC_N_MAX + 2 + 1;   // N+2 planes, rounded up to even
 constexpr int kMaxPairs = (kMaxPlanes + 1) / 2;
 constexpr int kMaxTemplW = 24;                 // FIR radius range with unrolled kernels
 constexpr int kMaxFirW = 1024;                 // runtime-W FIR kernels (taps in global)
-constexpr int kO1K = 6;                        // O(1) operator: cosine terms (q = 0 is the box)
+constexpr int kO1K = 5;                        // O(1) operator: cosine terms (q = 0 is the box); free-frequency fit
 constexpr int kO1MaxW = 4096;                  // O(1) operator radius limit
 constexpr int kO1AutoMinW = kMaxTemplW + 1;     // GC_OP_AUTO: FIR for W <= 24 (unrolled kernels), O(1) above
 

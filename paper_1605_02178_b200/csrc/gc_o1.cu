@@ -6,19 +6,21 @@
 // truncated window as the definition (R3) and reaches O(1) with an EXACT-WINDOW
 // recursion instead:
 //
-//   k_m ~= sum_{q=0}^{K-1} alpha_q cos(w_q m),   |m| <= W    (host least-squares fit, K = 6,
-//                                                             max error ~1e-6 of the peak tap)
+//   k_m ~= sum_{q=0}^{K-1} alpha_q cos(w_q m),   |m| <= W    (host fit, gc_operator.cpp: K = 5,
+//                                                             w_0 = 0 and four optimised frequencies,
+//                                                             max error ~5e-8 of the peak tap)
 //   S_q(i) = sum_{m=-W}^{W} cos(w_q m) x(i+m)                 (window sum, exactly W wide)
 //   S_q(i+1) - 2 cos(w_q) S_q(i) + S_q(i-1)
 //        = cos(w_q W) [x(i+W+1) + x(i-W-1)] - cos(w_q (W+1)) [x(i+W) + x(i-W)]
 //
 // evaluated in Reinsch's form (D = S(i) - S(i-1); D += -4 sin^2(w/2) S + input; S += D),
-// which keeps the fp32 rounding of the unit-circle resonator small for small w_q.  q = 0
-// is the plain box sum S_0(i+1) = S_0(i) + x(i+W+1) - x(i-W).  Each line segment starts
-// from a zero state 2W+1 samples early ("lead-in"), so no state crosses segment or task
-// boundaries and the result is a pure function of the window — the same truncated sum as
-// eq. (7), up to the fit error and fp32 rounding.  Per plane pair and sample: 30 packed
-// FP32x2 instructions, independent of sigma_s.
+// which keeps the fp32 rounding of the unit-circle resonator small for small w_q (all four
+// w_q W / pi lie in 0.87..3.80).  q = 0 is the plain box sum S_0(i+1) = S_0(i) + x(i+W+1) -
+// x(i-W).  The weights alpha_q are folded into the states, so the filtered value is their sum.
+// Each line segment starts from a zero state 2W+1 samples early ("lead-in"), so no state crosses
+// segment or task boundaries and the result is a pure function of the window — the same
+// truncated sum as eq. (7), up to the fit error and fp32 rounding.  Per plane pair and sample:
+// 24 packed FP32x2 instructions, independent of sigma_s.
 //
 //   k_row_o1 (a1 + a2, horizontal): warp = 32 image rows (lane = row) x one x-segment x
 //            <= 4 plane pairs; f is staged through a transposed shared-memory tile (coalesced
@@ -168,8 +170,8 @@ __device__ __forceinline__ void o1_update(const KParams& p, float2& S0, float2* 
 }
 
 __device__ __forceinline__ float2 o1_output(const KParams& p, float2 S0, const float2* S) {
-  static_assert(kO1K == 6, "o1_output's add tree assumes the box + 5 resonators");
-  return f2add(f2add(f2add(S0, S[0]), f2add(S[1], S[2])), f2add(S[3], S[4]));
+  static_assert(kO1K == 5, "o1_output's add tree assumes the box + 4 resonators");
+  return f2add(f2add(S0, S[0]), f2add(f2add(S[1], S[2]), S[3]));
 }
 
 template <int NPG>

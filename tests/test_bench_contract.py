@@ -38,12 +38,12 @@ def test_reference_arm_json_line():
 
 
 def test_flop_accounting():
-    """FIR: 2(2R+1) FLOP per plane-pixel and pass; O(1): 50; Deriche: 35 (N+2 planes)."""
+    """FIR: 2(2R+1) FLOP per plane-pixel and pass; O(1): 37; Deriche: 35 (N+2 planes)."""
     N, R, px = 8, 15, 1000
     assert bench.op_flop_per_plane(1, R) == 62
     assert bench.flops_row(N, R, px, 1) == px * (10 * 62 + 15)
     assert bench.flops_col(N, R, px, 1) == px * (10 * 62 + 6 * 9 + 8)
-    assert bench.flops_col(N, R, px, 2) == px * (10 * 50 + 6 * 9 + 8)
+    assert bench.flops_col(N, R, px, 2) == px * (10 * 37 + 6 * 9 + 8)
     assert bench.op_flop_per_plane(3, R) == 35
     assert bench.resolve_op(0, 24) == 1 and bench.resolve_op(0, 25) == 2 and bench.resolve_op(3, 5) == 3
 

@@ -79,6 +79,9 @@ def _args(argv=None):
     a.add_argument("--no-cpu-baseline", action="store_true")
     a.add_argument("--op", type=int, default=0, choices=[0, 1, 2, 3], help="0 auto, 1 FIR, 2 O(1), 3 Deriche (NOT eq. 7)")
     a.add_argument("--fp64", action="store_true", help="binary64 internal arithmetic (GC_PREC_FP64)")
+    a.add_argument("--force-bands", action="store_true",
+                   help="c5: run the row-band path (NCCL communicator, gc_bilateral_band) even at one rank "
+                        "(exercises the N > 1 code path on one GPU; the band is the whole image)")
     return a.parse_args(argv)
 
 
@@ -510,7 +513,12 @@ def main():
     import paper_1605_02178_b200 as gc
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
+    if ws > 1 or args.force_bands:
+        if ws == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(_free_port()))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
     R = math.ceil(3 * sigma_s)
     op = resolve_op(args.op, R) if not args.fp64 else 1
@@ -522,7 +530,7 @@ def main():
         mine = shard_of(cfg.batch, ws, rank)
         x = torch.from_numpy(np.stack([config_image(cfg, index=i) for i in mine])).to(dev)
         H, W, B = cfg.H, cfg.W, len(mine)
-    elif cfg.name == "c5" and ws > 1:
+    elif cfg.name == "c5" and (ws > 1 or args.force_bands):
         band_rows = band_rows_of(cfg.H, ws)
         pl = gc.band_plan(cfg.H, rank, ws, band_rows, sigma_s, op=args.op)
         row0 = pl["row0"]
@@ -675,7 +683,7 @@ def main():
     if rank != 0:
         if comm is not None:
             comm.close()
-        if ws > 1:
+        if dist.is_initialized():
             dist.destroy_process_group()
         return
     if rows_chk is not None:
@@ -714,7 +722,7 @@ def main():
         line["oracle_check"] = check
     if comm is not None:
         comm.close()
-    if ws > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     if not args.no_sweep and cfg.name == "c5":
         line["c3_sweep"] = c3_sweep(gc, dev, 10)

@@ -221,3 +221,51 @@ def test_out_buffer_checks_and_scratch_trim(gc):
     b = gc.filter(img, 3.0, 70.0, 8)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+# ------------------------------------------------------------------ pair-parallel column pass (k_col_o1p)
+
+@pytest.mark.parametrize("N,sigma_s,H,W", [
+    (0, 9.0, 37, 64),      # NP = 1 (one consumer warp)
+    (1, 2.0, 40, 62),      # NP = 2, lead-in of 8 (zl = 7: first leaving row inside the last lead-in stage)
+    (2, 1.0, 19, 34),      # NP = 2, W_s = 3
+    (3, 5.5, 61, 96),      # NP = 3, ragged last fold block
+    (4, 3.0, 9, 40),       # NP = 3, image shorter than the lead-in
+    (6, 16.0, 131, 98),    # NP = 4
+    (8, 12.5, 70, 130),    # NP = 5
+    (10, 7.0, 203, 66),    # NP = 6
+    (12, 16.0, 97, 160),   # NP = 7 (c5)
+    (13, 4.0, 50, 258),    # NP = 8: the largest pair-parallel kernel
+    (14, 20.0, 45, 66),    # NP = 8, W_s = 60 > H (repeated mirroring in y)
+])
+def test_pair_parallel_column_pass(gc, N, sigma_s, H, W):
+    """k_col_o1p (even widths, NP <= 8 plane pairs) for every NP, window lengths that are and are
+    not multiples of the 4-row stage / NP-row fold block, lead-ins longer than the image: GCF vs
+    the oracle (well-conditioned sigma_r = 200)."""
+    import torch
+    img = config_image("c2", H=H, W=W)
+    t = torch.from_numpy(img).cuda()
+    out = gc.filter(t, sigma_s, 200.0, N, op=OP_O1)
+    torch.cuda.synchronize()
+    ref, nfb = oracle.gc_filter(img, sigma_s, 200.0, N)
+    err = np.abs(out.cpu().numpy().astype(np.float64) - ref)
+    assert nfb == 0
+    assert err.max() <= MAX_ABS and math.sqrt(np.mean(err ** 2)) <= RMS, (N, sigma_s, H, W, err.max())
+
+
+@pytest.mark.parametrize("rows", [(0, 57), (57, 131), (131, 190), (40, 41)])
+def test_pair_parallel_column_pass_windows(gc, rows):
+    """Interior and edge row windows (gc_filter_window, the band path's building block) through
+    k_col_o1p: the producer's per-row boxes at window edges and its clamped entering rows."""
+    import torch
+    H, W, s = 190, 98, 16.0
+    img = config_image("c5", H=H, W=W)
+    R = math.ceil(3 * s)
+    r0, r1 = rows
+    a, b = max(0, r0 - R), min(H, r1 + R)
+    seg = torch.from_numpy(np.ascontiguousarray(img[a:b])).cuda()
+    out = gc.filter_window([(seg, a)], H, r0, r1 - r0, s, 200.0, 12, op=OP_O1)
+    torch.cuda.synchronize()
+    ref, _ = oracle.gc_filter_rows(img, list(range(r0, r1)), s, 200.0, 12)
+    err = np.abs(out.cpu().numpy().astype(np.float64) - ref)
+    assert err.max() <= MAX_ABS and math.sqrt(np.mean(err ** 2)) <= RMS, (rows, err.max())

@@ -159,13 +159,17 @@ __device__ __forceinline__ void o1_stage_row(const KParams& p, float2* t, float*
 __device__ __forceinline__ void o1_update(const KParams& p, float2& S0, float2* S, float2* D, float2 A, float2 B,
                                           float2 xin, float2 xout) {
   S0 = f2fma(f2s(p.o1_alpha[0]), f2sub(xin, xout), S0);
+  // (written stage by stage across the resonators: consecutive instructions are independent)
+  float2 d[kO1K - 1];
+#pragma unroll
+  for (int t = 0; t < kO1K - 1; t++) d[t] = f2fma(f2s(p.o1_nk[t + 1]), S[t], D[t]);
+#pragma unroll
+  for (int t = 0; t < kO1K - 1; t++) d[t] = f2fma(f2s(p.o1_a[t + 1]), A, d[t]);
 #pragma unroll
   for (int t = 0; t < kO1K - 1; t++) {
-    float2 d = f2fma(f2s(p.o1_nk[t + 1]), S[t], D[t]);
-    d = f2fma(f2s(p.o1_a[t + 1]), A, d);
-    d = f2fma(f2s(p.o1_nb[t + 1]), B, d);
-    D[t] = d;
-    S[t] = f2add(S[t], d);
+    d[t] = f2fma(f2s(p.o1_nb[t + 1]), B, d[t]);
+    D[t] = d[t];
+    S[t] = f2add(S[t], d[t]);
   }
 }
 
@@ -191,8 +195,54 @@ __device__ __forceinline__ void row_o1_step(const KParams& p, RowO1Smem& sm, Row
   if ((pl_pos & (kO1CH - 1)) == 0) o1_stage_row<1, PM>(p, sm.fout, sm.raw[1], rowp, pl_pos, lane, vec, p0);
   const float2 ve = sm.fin[lane * kO1TS + (pe_pos & (kO1CH - 1))];
   const float2 vl = sm.fout[lane * kO1TS + (pl_pos & (kO1CH - 1))];
-  float2 pe = make_float2(ve.x, ve.x * ve.y), pl = make_float2(vl.x, vl.x * vl.y);
   const float a2e = ve.y * ve.y, a2l = vl.y * vl.y;
+#ifndef GC_ROW_STAGED
+#define GC_ROW_STAGED 1
+#endif
+#if GC_ROW_STAGED
+  // The NPG pairs' updates interleaved by stage (all pairs' first FMA, then all second FMAs, ...):
+  // consecutive instructions are independent, so a warp can issue back to back instead of waiting
+  // on each resonator's 4-deep dependency chain (ncu r02: 'wait' was k_row_o1's top stall).
+  float2 pe[NPG], pl[NPG];
+  pe[0] = make_float2(ve.x, ve.x * ve.y);
+  pl[0] = make_float2(vl.x, vl.x * vl.y);
+#pragma unroll
+  for (int q = 1; q < NPG; q++) {
+    pe[q] = f2mul(pe[q - 1], f2s(a2e));
+    pl[q] = f2mul(pl[q - 1], f2s(a2l));
+  }
+#pragma unroll
+  for (int q = 0; q < NPG; q++) sm.o[q][j][lane] = o1_output(p, st.S0[q], st.S[q]);
+  float2 A[NPG], B[NPG], d[NPG][kO1K - 1];
+#pragma unroll
+  for (int q = 0; q < NPG; q++) {
+    A[q] = f2add(pe[q], st.Lp[q]);
+    B[q] = f2add(st.Ep[q], pl[q]);
+    st.S0[q] = f2fma(f2s(p.o1_alpha[0]), f2sub(pe[q], pl[q]), st.S0[q]);
+  }
+#pragma unroll
+  for (int t = 0; t < kO1K - 1; t++)
+#pragma unroll
+    for (int q = 0; q < NPG; q++) d[q][t] = f2fma(f2s(p.o1_nk[t + 1]), st.S[q][t], st.D[q][t]);
+#pragma unroll
+  for (int t = 0; t < kO1K - 1; t++)
+#pragma unroll
+    for (int q = 0; q < NPG; q++) d[q][t] = f2fma(f2s(p.o1_a[t + 1]), A[q], d[q][t]);
+#pragma unroll
+  for (int t = 0; t < kO1K - 1; t++)
+#pragma unroll
+    for (int q = 0; q < NPG; q++) {
+      d[q][t] = f2fma(f2s(p.o1_nb[t + 1]), B[q], d[q][t]);
+      st.D[q][t] = d[q][t];
+      st.S[q][t] = f2add(st.S[q][t], d[q][t]);
+    }
+#pragma unroll
+  for (int q = 0; q < NPG; q++) {
+    st.Ep[q] = pe[q];
+    st.Lp[q] = pl[q];
+  }
+#else
+  float2 pe = make_float2(ve.x, ve.x * ve.y), pl = make_float2(vl.x, vl.x * vl.y);
 #pragma unroll
   for (int q = 0; q < NPG; q++) {
     sm.o[q][j][lane] = o1_output(p, st.S0[q], st.S[q]);
@@ -202,6 +252,7 @@ __device__ __forceinline__ void row_o1_step(const KParams& p, RowO1Smem& sm, Row
     pe = f2mul(pe, f2s(a2e));
     pl = f2mul(pl, f2s(a2l));
   }
+#endif
 }
 
 template <int NPG, int PM>

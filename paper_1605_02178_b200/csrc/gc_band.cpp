@@ -14,6 +14,7 @@
 #include <vector>
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "gc_internal.h"
 
@@ -151,6 +152,9 @@ gc_status gc_filter_band(const float* band, int H_band, int W, int H_global, int
       return GC_ENOMEM;
     }
   }
+  // NVTX ranges (header-only nvtx3; no-ops unless a profiler is attached): the host-side enqueue of
+  // the halo exchange and of the band's two filter passes, for nsys / ncu --nvtx
+  nvtxRangePushA("gc.band.exchange");
   if (ncclGroupStart() != ncclSuccess) st = GC_ENCCL;
   for (int k = 0; k < 2 && st == GC_OK; k++) {
     if (x[k].peer < 0) continue;
@@ -158,9 +162,12 @@ gc_status gc_filter_band(const float* band, int H_band, int W, int H_global, int
     if (ncclRecv(recv[k], x[k].count, ncclFloat32, x[k].peer, c, s) != ncclSuccess) st = GC_ENCCL;
   }
   if (ncclGroupEnd() != ncclSuccess) st = GC_ENCCL;
+  nvtxRangePop();
   if (st == GC_OK) {
+    nvtxRangePushA("gc.band.filter");
     const float* seg[3] = {recv[0] ? recv[0] : band, band, recv[1] ? recv[1] : band};
     st = gc_filter_window(seg, seg_row0, seg_rows, H_global, W, row0, H_band, p, out, stream);
+    nvtxRangePop();
   }
   if (recv[0]) cudaFreeAsync(recv[0], s);
   if (recv[1]) cudaFreeAsync(recv[1], s);

@@ -61,6 +61,28 @@ struct RowO1Smem {
   float raw[2][32 * kO1RS];                // f of the NEXT chunk of each stream (cp.async prefetch)
 };
 
+// L2 cache policies (createpolicy): streaming data that is not read again in this kernel (plane
+// stores of the row pass, the output) is marked evict_first so it does not push out what is
+// (f, re-read by the leaving stream and the other pair group; the column pass's window rows).
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ unsigned long long l2_evict_last() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_f2_hint(float2* a, float2 v, unsigned long long pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(a), "f"(v.x), "f"(v.y),
+               "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_f_hint(float* a, float v, unsigned long long pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
+}
+
 // Prefetch f of this lane's row at the 16 positions [pc, pc+16) (whole-sample mirroring in x)
 // into raw (one cp.async group per call): the stage one chunk later finds it in shared memory
 // instead of stalling on DRAM (ncu r01: long_scoreboard was the top stall of k_row_o1).
@@ -73,7 +95,9 @@ __device__ __forceinline__ void o1_prefetch_row(const KParams& p, float* raw, co
     for (int k = 0; k < kO1CH / 4; k++)
     {
       GC_CHK(p, rowp + pc + 4 * k, 16);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s + 16 * k), "l"(rowp + pc + 4 * k) : "memory");
+      asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(s + 16 * k),
+                   "l"(rowp + pc + 4 * k), "l"(l2_evict_last())
+                   : "memory");
     }
   } else {
 #pragma unroll 1
@@ -301,6 +325,7 @@ __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int
   const int rows_left = p.in_rows - (r0 + orow);            // rows r0+orow+ORS j valid for ORS j < rows_left
   float2* const obase = p.planes + b * p.planes_img_stride + (long long)(r0 + orow) * rstride +
                         (long long)p0 * p.Wd + ocol;
+  const unsigned long long pol_stream = l2_evict_first();
 #pragma unroll 1
   for (int x = xs; x < xe; x += kO1OC) {
     const int nb = min(kO1OC, xe - x);
@@ -316,7 +341,7 @@ __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int
         for (int j = 0; j < 32 / ORS; j++)
           if (ORS * j < rows_left) {
             GC_CHK(p, &o[(long long)(ORS * j) * rstride], 8);
-            o[(long long)(ORS * j) * rstride] = sm.o[q][ocol][ORS * j + orow];
+            st_f2_hint(&o[(long long)(ORS * j) * rstride], sm.o[q][ocol][ORS * j + orow], pol_stream);
           }
         o += p.Wd;
       }
@@ -814,6 +839,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
   }
   float* const outp = p.out + b * p.out_img_stride + x;
   unsigned nguard = 0;
+  const unsigned long long pol_out = l2_evict_first();
   const unsigned tf0 = smem_u32(&sm.tile_full[0]), tr0 = smem_u32(&sm.tile_free[0]);
   // Blocks of NP output rows: block blk is filtered into tile buffer blk & 1 while block blk-1 is
   // folded (eqs. 8-10) from the other buffer, warp q folding row q — every warp does the same work
@@ -888,7 +914,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
             nguard++;
           }
           GC_CHK(p, &outp[(long long)(pbs + q) * p.Wd], 4);
-          outp[(long long)(pbs + q) * p.Wd] = o;
+          st_f_hint(&outp[(long long)(pbs + q) * p.Wd], o, pol_out);
         }
       }
       __syncwarp();

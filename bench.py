@@ -195,7 +195,7 @@ def roofline(N, R, op, px, row_ms, col_ms, step_ms, traffic_key=None):
 
 class ClockSampler:
     def __init__(self, index=0, period=0.005):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.samples, self.reasons, self.max_mhz, self.power_w = [], set(), None, []
         self.period, self.index = period, index
         self._stop = threading.Event()
         self._t = None
@@ -220,6 +220,10 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    self.power_w.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+                except Exception:
+                    pass
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in names.items():
                     if isinstance(bit, int) and bit and (r & bit) == bit:
@@ -237,7 +241,9 @@ class ClockSampler:
         s = sorted(self.samples)
         med = s[len(s) // 2] if s else None
         bad = [r for r in self.reasons if r not in ("All", "None", "Unknown", "GpuIdle")]
-        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "samples": len(s), "reasons": sorted(bad)}
+        pw = sorted(self.power_w)
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "samples": len(s), "reasons": sorted(bad),
+                "power_w_median": pw[len(pw) // 2] if pw else None}
 
 
 # ------------------------------------------------------------------ CPU oracle (cpu_baseline and --impl reference)
@@ -712,11 +718,18 @@ def main():
     hbm = {"algorithmic_bytes_per_px": 8, "achieved_GBps": 8 * px_rank / (ms_step / 1e3) / 1e9,
            "peak_GBps": HBM_PEAK_GBPS, "peak_source": HBM_PEAK_SOURCE}
     hbm["frac_of_measured"] = hbm["achieved_GBps"] / HBM_PEAK_GBPS
+    csum = clk.summary()
+    energy = None
+    if csum.get("power_w_median"):
+        # board power during the timed region x step time / pixels of the step (this GPU's share)
+        energy = {"J_per_Mpx": csum["power_w_median"] * (ms_step / 1e3) / (px_rank / 1e6),
+                  "note": "median NVML board power during the timed region; the step is power-capped when "
+                          "clocks.reasons lists SwPowerCap"}
     line = {"metric": METRIC, "value": value, "unit": "MP/s", "n_gpus": ws, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": _scaling(cfg), "vs_baseline": None,
             "dtype": "f64" if args.fp64 else "f32", "data": "synthetic (seeded, synth/images.py)",
             "config": _config(cfg, sigma_s, sigma_r, ws), "roofline": roof, "kernels": kernels, "hbm": hbm,
-            "e2e": e2e, "gpu_launches": 2 * K, "clocks": clk.summary(), "impl": "ours", "lib": gc.version(),
+            "e2e": e2e, "gpu_launches": 2 * K, "clocks": csum, "energy": energy, "impl": "ours", "lib": gc.version(),
             "host_cores": len(os.sched_getaffinity(0)), "input_generation_s": gen_s}
     if check is not None:
         line["oracle_check"] = check

@@ -58,6 +58,36 @@ void o1_constants(float sigma_s, KParams& k) {
   }
 }
 
+// Direct lead-in table of the row pass (KParams::o1_lead): the window sums of the alpha-folded
+// resonator states at a segment's first output, written out as dot products with the taps
+// alpha_q cos(w_q m) of the fit.  Empty when GC_O1_DIRECT_LEAD=0 (recursion lead-in, A/B).
+std::vector<float4> o1_lead_table(float sigma_s, int W) {
+  static const bool on = [] {
+    const char* v = std::getenv("GC_O1_DIRECT_LEAD");
+    return !(v && v[0] == '0');
+  }();
+  if (!on) return {};
+  const O1Fit f = o1_fit_cached(sigma_s);
+  if (f.R != W) return {};
+  static_assert(kO1K == 5, "the lead-in table packs the 4 resonators into one float4");
+  const int R = f.R;
+  std::vector<float4> t(2 * (2 * R + 1));
+  for (int s = 0; s <= 2 * R; s++) {
+    const int m = s - R;
+    double c[4], d[4];
+    for (int q = 0; q < 4; q++) {
+      const double a = f.alpha[q + 1], w = f.omega[q + 1];
+      c[q] = a * std::cos(w * m);
+      // D = S(x) - S(x-1) of the zero-extended signal: tap m of the window at x minus tap m+1
+      // of the window at x-1 (which ends at m = W)
+      d[q] = m < R ? a * (std::cos(w * m) - std::cos(w * (m + 1))) : c[q];
+    }
+    t[2 * s] = make_float4((float)c[0], (float)c[1], (float)c[2], (float)c[3]);
+    t[2 * s + 1] = make_float4((float)d[0], (float)d[1], (float)d[2], (float)d[3]);
+  }
+  return t;
+}
+
 gc_status validate_params(const gc_params* p) {
   if (!p) return GC_EINVAL;
   if (p->N < 0) return GC_EINVAL;
@@ -267,10 +297,24 @@ gc_status run(KParams& k, const std::vector<float2>& taps_host, cudaStream_t s) 
   const size_t elem = k.fp64 ? sizeof(double2) : sizeof(float2);
   // (Deriche mode: a second plane-sized buffer after the counters for the causal partial sums)
   const size_t scratch_elems = op == GC_OP_DERICHE ? plane_elems * k.B : 0;
-  cudaError_t e = scratch_alloc((void**)&planes, plane_elems * k.B * elem + 256 + scratch_elems * elem, s);
+  // (O(1) mode: the direct lead-in table after the counters)
+  const std::vector<float4> lead = op == GC_OP_O1 && !k.fp64 ? o1_lead_table(k.sigma_s_host, k.R) : std::vector<float4>();
+  const size_t lead_bytes = lead.size() * sizeof(float4);
+  const size_t base_bytes = (plane_elems * k.B * elem + 256 + scratch_elems * elem + 255) / 256 * 256;
+  cudaError_t e = scratch_alloc((void**)&planes, base_bytes + lead_bytes, s);
   if (e != cudaSuccess) return cuda_status(e);
   k.counters = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(planes) + plane_elems * k.B * elem);
-  k.planes_bytes = plane_elems * k.B * elem + 256 + scratch_elems * elem;
+  k.planes_bytes = base_bytes + lead_bytes;
+  k.o1_lead = nullptr;
+  if (lead_bytes) {
+    float4* lead_dev = reinterpret_cast<float4*>(reinterpret_cast<char*>(planes) + base_bytes);
+    e = cudaMemcpyAsync(lead_dev, lead.data(), lead_bytes, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(planes, s);
+      return cuda_status(e);
+    }
+    k.o1_lead = lead_dev;
+  }
   k.oob = oob_counter();
   k.scratch = scratch_elems ? reinterpret_cast<float2*>(reinterpret_cast<char*>(k.counters) + 256) : nullptr;
   if (k.fp64 || (op == GC_OP_FIR && k.R > kMaxTemplW)) {

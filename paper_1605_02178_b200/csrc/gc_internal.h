@@ -80,6 +80,10 @@ struct KParams {
   int o1_seg_y, o1_nseg_y;         // column pass: y-segment length and count
   int o1_groups;                   // row pass: plane-pair groups (<= 4 pairs each)
   int o1_stages;                   // pair-parallel column pass: TMA ring stages
+  // direct lead-in (row pass): for s = 0..2W, m = s - W, two float4 per s:
+  // {alpha_q cos(w_q m)}_{q=1..4} and {alpha_q (cos(w_q m) - cos(w_q (m+1)))} (the m = W entry
+  // without its cos(w_q (W+1)) term); null = lead the recursion in from a zero state instead
+  const float4* o1_lead;
   int raw;                         // 1: eq. (7) of f itself (gc_gaussian): pair 0 = (f, 0), out = Fbar_0
   // Deriche-class recursive operator (gc_deriche.cu; GC_OP_DERICHE): two 2nd-order sections per
   // direction, 1/Z folded into b0, b1, c1, c2

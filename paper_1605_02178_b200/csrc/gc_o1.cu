@@ -295,23 +295,59 @@ __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int
   const float* rowp = row_ptr(p, b, p.in_row0 + min(r0 + lane, p.in_rows - 1));
   const bool vec = ((p.Wd & 3) == 0) && ((reinterpret_cast<uintptr_t>(rowp) & 15) == 0);
 
-  // ---- lead-in: windows xs-2W-1 .. xs-1 (leaving samples are still zero)
+  // ---- lead-in: the state at the first output x = xs from the 2W+1 samples of its window
   o1_prefetch_row(p, sm.raw[0], rowp, P0 & ~(kO1CH - 1), lane, vec);
   o1_prefetch_row(p, sm.raw[1], rowp, (xs - R) & ~(kO1CH - 1), lane, vec);
+  const float4* const lt = p.o1_lead;
+  // chunk by chunk (one staging per chunk), the samples of a chunk unrolled: their latency
+  // chains (shared-memory load, the a^2 power chain across the pairs) overlap
 #pragma unroll 1
-  for (int s = 0; s < lead; s++) {
-    const int pos = P0 + s;
-    if (s == 0 || (pos & (kO1CH - 1)) == 0)      // (only this stream stages here: wait for all groups)
-      o1_stage_row<0, PM>(p, sm.fin, sm.raw[0], rowp, pos & ~(kO1CH - 1), lane, vec, p0);
-    const float2 ve = sm.fin[lane * kO1TS + (pos & (kO1CH - 1))];
-    float2 pe = make_float2(ve.x, ve.x * ve.y);
-    const float a2e = ve.y * ve.y;
+  for (int s0 = 0; s0 < lead;) {
+    const int pos0 = P0 + s0;
+    // (only this stream stages here: wait for all groups)
+    o1_stage_row<0, PM>(p, sm.fin, sm.raw[0], rowp, pos0 & ~(kO1CH - 1), lane, vec, p0);
+    const int n = min(kO1CH - (pos0 & (kO1CH - 1)), lead - s0);
+    if (lt) {
+      // direct: S_q(xs) and D_q(xs) = S_q(xs) - S_q(xs-1) as dot products with the fitted taps
+      // (the state the recursion reaches from a zero state after these 2W+1 steps, with 9
+      // instead of 17 packed operations per pair and sample)
+#pragma unroll 4
+      for (int i = 0; i < n; i++) {
+        const int s = s0 + i;
+        const float2 ve = sm.fin[lane * kO1TS + ((pos0 + i) & (kO1CH - 1))];
+        float2 pe = make_float2(ve.x, ve.x * ve.y);
+        const float a2e = ve.y * ve.y;
+        GC_CHK(p, &lt[2 * s], 32);
+        const float4 c = __ldg(&lt[2 * s]), d = __ldg(&lt[2 * s + 1]);
+        const float cq[4] = {c.x, c.y, c.z, c.w}, dq[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
-    for (int q = 0; q < NPG; q++) {
-      o1_update(p, st.S0[q], st.S[q], st.D[q], pe, st.Ep[q], pe, make_float2(0.f, 0.f));
-      st.Ep[q] = pe;
-      pe = f2mul(pe, f2s(a2e));
+        for (int q = 0; q < NPG; q++) {
+          st.S0[q] = f2fma(f2s(p.o1_alpha[0]), pe, st.S0[q]);
+#pragma unroll
+          for (int t = 0; t < kO1K - 1; t++) {
+            st.S[q][t] = f2fma(f2s(cq[t]), pe, st.S[q][t]);
+            st.D[q][t] = f2fma(f2s(dq[t]), pe, st.D[q][t]);
+          }
+          st.Ep[q] = pe;
+          pe = f2mul(pe, f2s(a2e));
+        }
+      }
+    } else {
+      // recursion from a zero state over windows xs-2W-1 .. xs-1 (leaving samples still zero)
+#pragma unroll 1
+      for (int i = 0; i < n; i++) {
+        const float2 ve = sm.fin[lane * kO1TS + ((pos0 + i) & (kO1CH - 1))];
+        float2 pe = make_float2(ve.x, ve.x * ve.y);
+        const float a2e = ve.y * ve.y;
+#pragma unroll
+        for (int q = 0; q < NPG; q++) {
+          o1_update(p, st.S0[q], st.S[q], st.D[q], pe, st.Ep[q], pe, make_float2(0.f, 0.f));
+          st.Ep[q] = pe;
+          pe = f2mul(pe, f2s(a2e));
+        }
+      }
     }
+    s0 += n;
   }
   // ---- outputs x = xs .. xe-1, in chunks of kO1OC positions (xs is a multiple of 32).  The
   // leaving stream's first chunk: staged here unless x = xs itself starts a chunk (then the first
@@ -351,41 +387,59 @@ __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int
   asm volatile("cp.async.wait_group 0;" ::: "memory");      // no copy may land after the task
 }
 
-__global__ void __launch_bounds__(32 * kO1Warps, 3) k_row_o1(const KParams p) {
+// Task decode of the row pass: groups of kO1RowNPG plane pairs and one remainder group last,
+// tasks numbered group-major so that the dynamic fetch runs every task of the full groups before
+// the smaller one (longest-processing-time-first: the tail is short tasks).  (Balanced groups,
+// NP = 6 as 3 + 3 instead of 4 + 2, measured slower: r02ai.)
+struct RowO1Task {
+  int b, rb, sx, p0, npl;
+};
+__device__ __forceinline__ RowO1Task row_o1_decode(const KParams& p, int task, int nrb) {
+  const int per_group = nrb * p.o1_nseg_x * p.B;
+  const int g = task / per_group, rest = task - g * per_group;
+  RowO1Task t;
+  t.sx = rest % p.o1_nseg_x;
+  t.rb = (rest / p.o1_nseg_x) % nrb;
+  t.b = rest / (p.o1_nseg_x * nrb);
+  t.p0 = g * kO1RowNPG;
+  t.npl = min(kO1RowNPG, p.NP - t.p0);
+  return t;
+}
+
+// Persistent: one CTA per resident slot, each warp fetching tasks (32 rows x one x-segment x one
+// plane-pair group) from a counter that the launch zeroes, until none is left.
+__global__ void __launch_bounds__(32 * kO1Warps, 3) k_row_o1(const KParams p, unsigned* task_ctr) {
   extern __shared__ float4 smem_o1r[];
   pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   RowO1Smem& sm = reinterpret_cast<RowO1Smem*>(smem_o1r)[warp];
   const int nrb = (p.in_rows + 31) / 32;
   const int ntask = nrb * p.o1_nseg_x * p.o1_groups * p.B;
-  const int task = blockIdx.x * kO1Warps + warp;
-  if (task >= ntask) return;
-  // plane-pair group: rotated with the CTA index so that every SM sub-partition (warp % 4) gets
-  // a mix of the large and small groups (NP = 7: 4 + 3 pairs) instead of always the same one
-  const int rest = task / p.o1_groups;
-  const int g = (task % p.o1_groups + rest * p.o1_groups / kO1Warps) % p.o1_groups;
-  const int sx = rest % p.o1_nseg_x;
-  const int rb = (rest / p.o1_nseg_x) % nrb;
-  const int b = rest / (p.o1_nseg_x * nrb);
-  const int xs = sx * p.o1_seg_x, xe = min(xs + p.o1_seg_x, p.Wd);
-  const int p0 = g * kO1RowNPG;
-  const int npl = min(kO1RowNPG, p.NP - p0);
-  if (p.raw) {                                   // gc_gaussian: one pair (f, 0)
-    row_o1_task<1, kPmRaw>(p, sm, b, rb * 32, xs, xe, p0, lane);
-    return;
-  }
-  auto go = [&](auto pm) {
-    constexpr int PM = decltype(pm)::value;
-    switch (npl) {
-      case 1: row_o1_task<1, PM>(p, sm, b, rb * 32, xs, xe, p0, lane); break;
-      case 2: row_o1_task<2, PM>(p, sm, b, rb * 32, xs, xe, p0, lane); break;
-      case 3: row_o1_task<3, PM>(p, sm, b, rb * 32, xs, xe, p0, lane); break;
-      default: row_o1_task<4, PM>(p, sm, b, rb * 32, xs, xe, p0, lane); break;
+#pragma unroll 1
+  for (;;) {
+    int task = 0;
+    if (lane == 0) task = (int)atomicAdd(task_ctr, 1u);
+    task = __shfl_sync(0xffffffffu, task, 0);
+    if (task >= ntask) break;
+    const RowO1Task t = row_o1_decode(p, task, nrb);
+    const int xs = t.sx * p.o1_seg_x, xe = min(xs + p.o1_seg_x, p.Wd);
+    if (p.raw) {                                   // gc_gaussian: one pair (f, 0)
+      row_o1_task<1, kPmRaw>(p, sm, t.b, t.rb * 32, xs, xe, 0, lane);
+      continue;
     }
-  };
-  if (p0 == 0) go(std::integral_constant<int, kPm0>());
-  else if (p0 == 4) go(std::integral_constant<int, kPm4>());
-  else go(std::integral_constant<int, kPmAny>());
+    auto go = [&](auto pm) {
+      constexpr int PM = decltype(pm)::value;
+      switch (t.npl) {
+        case 1: row_o1_task<1, PM>(p, sm, t.b, t.rb * 32, xs, xe, t.p0, lane); break;
+        case 2: row_o1_task<2, PM>(p, sm, t.b, t.rb * 32, xs, xe, t.p0, lane); break;
+        case 3: row_o1_task<3, PM>(p, sm, t.b, t.rb * 32, xs, xe, t.p0, lane); break;
+        default: row_o1_task<4, PM>(p, sm, t.b, t.rb * 32, xs, xe, t.p0, lane); break;
+      }
+    };
+    if (t.p0 == 0) go(std::integral_constant<int, kPm0>());
+    else if (t.p0 == 4) go(std::integral_constant<int, kPm4>());
+    else go(std::integral_constant<int, kPmAny>());
+  }
 }
 
 // ------------------------------------------------------------------ column pass + eqs. (8)-(10)
@@ -825,7 +879,8 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
     if (lane == 0) o1_mbar_arrive(&sm.empty[st]);
     if (++st == nst) { st = 0; ph ^= 1; }
   };
-  // lead-in: whole stages, no output; leaving samples real from step zl on
+  // lead-in: whole stages, no output; leaving samples real from step zl on.  (The direct lead-in
+  // of the row pass measured no faster here, r02al: this loop waits on the TMA ring anyway.)
 #pragma unroll 1
   for (int k0 = 0; k0 < lead; k0 += kRPS) {
     acquire();
@@ -1056,11 +1111,33 @@ cudaError_t launch_o1_two_pass(const KParams& p0, cudaStream_t s) {
   KParams p = p0;
   p.o1_groups = (p.NP + kO1RowNPG - 1) / kO1RowNPG;
   const long long nrb = (p.in_rows + 31) / 32;
-  pick_segments(p.Wd, nrb * p.o1_groups * p.B, 2 * p.R + 1, resident_r.load(), 32, p.o1_seg_x, p.o1_nseg_x);
+  {
+    // x-segments: 16 per line, or one task per resident warp if that is more (the dynamic
+    // fetch balances the tasks), but segments at least twice the 2W+1 lead-in (measured: c5 and
+    // c3 sigma_s = 2 / 10 best at 16, c3 sigma_s = 40 at 8 = the lead-in bound; r02ai-ak)
+    const long long base = nrb * p.o1_groups * p.B, res = resident_r.load();
+    long long n = std::max<long long>(16, (res + base - 1) / base);
+    n = std::min<long long>(n, std::max(1, p.Wd / (2 * (2 * p.R + 1))));
+    n = std::max<long long>(1, std::min<long long>(n, (p.Wd + 31) / 32));
+    p.o1_seg_x = (int)(((p.Wd + n - 1) / n + 31) / 32 * 32);
+    p.o1_nseg_x = (p.Wd + p.o1_seg_x - 1) / p.o1_seg_x;
+  }
+  static const int force_nseg = [] {                 // A/B switch (development)
+    const char* v = std::getenv("GC_O1_ROW_NSEG");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (force_nseg > 0) {
+    p.o1_seg_x = ((p.Wd + force_nseg - 1) / force_nseg + 31) / 32 * 32;
+    p.o1_nseg_x = (p.Wd + p.o1_seg_x - 1) / p.o1_seg_x;
+  }
   const long long ntr = nrb * p.o1_nseg_x * p.o1_groups * p.B;
+  const long long row_ctas = std::min((ntr + kO1Warps - 1) / kO1Warps, resident_r.load() / kO1Warps);
+  unsigned* const row_ctr = p.counters + 1;          // (counters[0]: the FIR column pass)
   if (p.ev[0]) cudaEventRecord(p.ev[0], s);
-  row_kern<<<(unsigned)((ntr + kO1Warps - 1) / kO1Warps), 32 * kO1Warps, smem_r, s>>>(p);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = cudaMemsetAsync(row_ctr, 0, sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+  row_kern<<<(unsigned)std::max(1ll, row_ctas), 32 * kO1Warps, smem_r, s>>>(p, row_ctr);
+  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (p.ev[1]) cudaEventRecord(p.ev[1], s);
   // column pass: the pair-parallel kernel (NP <= 8, even width: TMA boxes), else G lanes per

@@ -1077,7 +1077,27 @@ cudaError_t launch_colp(const KParams& p0, cudaStream_t s) {
   p.o1_stages = nst;
 
   const long long ncb = (p.Wd + 31) / 32;
-  pick_segments(p.out_rows, ncb * p.B, 2 * p.R + 1, (long long)blocks * p.num_sms, 1, p.o1_seg_y, p.o1_nseg_y);
+  {
+    // y-segments: 8 per column strip (or one CTA per resident slot if that is more), none
+    // shorter than twice the lead-in (r02am sweep: c3 sigma_s = 10 / 20 / 40 column pass
+    // 0.442 / 0.504 / 0.528 ms with pick_segments' wave model, 0.438 / 0.463 / 0.512 at 8;
+    // c5 unchanged)
+    const long long base = ncb * p.B, res = (long long)blocks * p.num_sms;
+    const long long lead = (2 * p.R + 1 + kRPS - 1) / kRPS * kRPS;
+    long long n = std::max<long long>(8, (res + base - 1) / base);
+    n = std::min<long long>(n, std::max<long long>(1, p.out_rows / (2 * lead)));
+    n = std::max<long long>(1, std::min<long long>(n, p.out_rows));
+    p.o1_seg_y = (int)((p.out_rows + n - 1) / n);
+    p.o1_nseg_y = (p.out_rows + p.o1_seg_y - 1) / p.o1_seg_y;
+  }
+  static const int force_nseg = [] {                 // A/B switch (development)
+    const char* v = std::getenv("GC_O1_COL_NSEG");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (force_nseg > 0) {
+    p.o1_seg_y = (p.out_rows + force_nseg - 1) / force_nseg;
+    p.o1_nseg_y = (p.out_rows + p.o1_seg_y - 1) / p.o1_seg_y;
+  }
   const long long nt = ncb * p.o1_nseg_y * p.B;
   return launch_k(kern, dim3((unsigned)nt), dim3(32 * (NP + 1)), smem, s, p.ev[1] == nullptr, map, map4, p);
 }

@@ -389,8 +389,9 @@ __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int
 
 // Task decode of the row pass: groups of kO1RowNPG plane pairs and one remainder group last,
 // tasks numbered group-major so that the dynamic fetch runs every task of the full groups before
-// the smaller one (longest-processing-time-first: the tail is short tasks).  (Balanced groups,
-// NP = 6 as 3 + 3 instead of 4 + 2, measured slower: r02ai.)
+// the smaller one (longest-processing-time-first: the tail is short tasks).  (Measured slower:
+// balanced groups, NP = 6 as 3 + 3 instead of 4 + 2, r02ai; the groups of one segment adjacent
+// so that they share f in L2, r02ap: c5 row 4.78 -> 5.01 ms.)
 struct RowO1Task {
   int b, rb, sx, p0, npl;
 };

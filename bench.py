@@ -159,15 +159,22 @@ def flops_col(N, R, px, op=1):
     return px * ((N + 2) * op_flop_per_plane(op, R) + 6 * (N + 1) + 8)
 
 
-def roofline(N, R, op, px, row_ms, col_ms, step_ms, traffic_key=None):
+def roofline(N, R, op, px, row_ms, col_ms, step_ms, traffic_key=None, fused=False):
     """Roofline of the dominant kernel: `achieved`/`frac` on SURVEY §8(d)'s
     algorithmic instruction count against the derived FP32 ALU peak; `design` = the same kernel's
-    implemented FLOP against 74.45 TFLOP/s; `step_frac` = the whole step on the algorithmic count."""
+    implemented FLOP against 74.45 TFLOP/s; `step_frac` = the whole step on the algorithmic count.
+    fused: the call ran as the one small-image FIR kernel (gc_filter_kernels == 1, csrc/gc_fused.cu),
+    timed by the first event interval; the second is then empty."""
     alg = alg_instr(N)
-    dom = "k_col" if col_ms >= row_ms else "k_row"
-    ms = {"k_row": row_ms, "k_col": col_ms}[dom]
+    if fused:
+        # the small-image FIR path (csrc/gc_fused.cu): one kernel does both passes and eqs. (8)-(10)
+        dom, ms, alg = "k_fused_fir", row_ms, dict(alg, k_fused_fir=alg["total"])
+        design = (flops_row(N, R, px, op) + flops_col(N, R, px, op)) / (ms / 1e3) / 1e12
+    else:
+        dom = "k_col" if col_ms >= row_ms else "k_row"
+        ms = {"k_row": row_ms, "k_col": col_ms}[dom]
+        design = (flops_col if dom == "k_col" else flops_row)(N, R, px, op) / (ms / 1e3) / 1e12
     ach = alg[dom] * px / (ms / 1e3) / 1e12
-    design = (flops_col if dom == "k_col" else flops_row)(N, R, px, op) / (ms / 1e3) / 1e12
     out = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": FP32_PEAK_TINSTR,
            "unit": "T FP32 instr/s (SURVEY §8(d) algorithmic count)", "frac": ach / FP32_PEAK_TINSTR,
            "alg_instr_per_px": alg[dom], "units_per_launch": px, "peak_source": PEAK_SOURCE,
@@ -552,6 +559,10 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if cfg.name in ("c1", "c2", "c3") else None
     stream = torch.cuda.current_stream()
 
+    # kernels per step as libgc reports them (1 = the fused small-image FIR kernel)
+    n_kern = 2 if comm is not None else gc.filter_kernels(B, H, W, sigma_s, sigma_r, cfg.N, op=args.op, fp64=args.fp64)
+    fused = n_kern == 1
+
     def step(events=None, sr=sigma_r, dst=out):
         if comm is not None:
             gc.bilateral_band(x, cfg.H, row0, sigma_s, sr, cfg.N, comm, out=dst, op=args.op, events=events)
@@ -701,10 +712,13 @@ def main():
     roof = kernels = None
     if row_ms is not None:
         key = f"{cfg.name}_s{sigma_s:g}_{ {1: 'fir', 2: 'o1', 3: 'deriche'}[op]}" + (f"_g{ws}" if comm else "")
-        roof = roofline(cfg.N, R, op, px_rank, row_ms, col_ms, ms_step, traffic_key=key)
+        roof = roofline(cfg.N, R, op, px_rank, row_ms, col_ms, ms_step, traffic_key=key, fused=fused)
         fr, fc = flops_row(cfg.N, R, px_rank, op), flops_col(cfg.N, R, px_rank, op)
-        kernels = {"k_row": {"ms": row_ms, "design_tflops": fr / row_ms / 1e9},
-                   "k_col": {"ms": col_ms, "design_tflops": fc / col_ms / 1e9}}
+        if fused:
+            kernels = {"k_fused_fir": {"ms": row_ms, "design_tflops": (fr + fc) / row_ms / 1e9}}
+        else:
+            kernels = {"k_row": {"ms": row_ms, "design_tflops": fr / row_ms / 1e9},
+                       "k_col": {"ms": col_ms, "design_tflops": fc / col_ms / 1e9}}
         if comm is not None:
             kernels["halo_exchange"] = {"ms": xchg_ms, "bytes_per_neighbour": R * W * 4}
         if op == 3:                                # Deriche mode: the design's HBM bytes too
@@ -729,7 +743,7 @@ def main():
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": _scaling(cfg), "vs_baseline": None,
             "dtype": "f64" if args.fp64 else "f32", "data": "synthetic (seeded, synth/images.py)",
             "config": _config(cfg, sigma_s, sigma_r, ws), "roofline": roof, "kernels": kernels, "hbm": hbm,
-            "e2e": e2e, "gpu_launches": 2 * K, "clocks": csum, "energy": energy, "impl": "ours", "lib": gc.version(),
+            "e2e": e2e, "gpu_launches": n_kern * K, "clocks": csum, "energy": energy, "impl": "ours", "lib": gc.version(),
             "host_cores": len(os.sched_getaffinity(0)), "input_generation_s": gen_s}
     if check is not None:
         line["oracle_check"] = check

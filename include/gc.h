@@ -149,6 +149,18 @@ gc_status gc_filter(const float* imgs, int B, int H, int W, const gc_params* p, 
                     void* stream);
 
 /*
+ * gc_filter_kernels — the number of kernels gc_filter(imgs, B, H, W, p, ...) launches on its
+ * stream, without launching anything (host only): 1 when the call takes the small-image fused
+ * FIR kernel (operator FIR, W_s <= 24, B*H*W at most GC_FUSED_MAX_PX output pixels: both passes
+ * of eq. (7) P:92-96 and eqs. (8)-(10) in one launch, csrc/gc_fused.cu), else 2 (the two passes;
+ * the O(1) path also zeroes a 4-byte task counter with a memset node).  With p->events set, a
+ * fused call records events[0] before and events[1], events[2] after its one kernel.
+ * Errors: GC_EINVAL / GC_ERANGE as gc_filter's parameter checks, GC_EINVAL for a null n_kernels.
+ */
+#define GC_FUSED_MAX_PX (1 << 18)
+gc_status gc_filter_kernels(int B, int H, int W, const gc_params* p, int* n_kernels);
+
+/*
  * gc_filter_host — end-to-end call on HOST buffers (pinned memory recommended):
  * copies imgs (B*H*W fp32) host->device, filters, copies the result device->host into
  * outs, all on `stream`, and returns after synchronising that stream (so outs is

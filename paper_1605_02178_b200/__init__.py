@@ -19,6 +19,7 @@ __all__ = [
     "filter_host", "filter_window", "band_plan", "Comm", "bilateral_band", "version",
     "OP_AUTO", "OP_FIR", "OP_O1", "OP_DERICHE", "gaussian", "operator_taps", "bilateral_direct",
     "band_exchange_plan", "filter_band", "scratch_trim", "debug_oob_count", "debug_oob_selftest",
+    "filter_kernels",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -78,6 +79,7 @@ def _lib():
         L.gc_params_init.restype = None
         L.gc_filter.argtypes = [vp, i, i, i, ctypes.POINTER(_Params), vp, vp]
         L.gc_filter_host.argtypes = [vp, i, i, i, ctypes.POINTER(_Params), vp, vp]
+        L.gc_filter_kernels.argtypes = [i, i, i, ctypes.POINTER(_Params), ip]
         L.gc_filter_window.argtypes = [ctypes.POINTER(vp), ip, ip, i, i, i, i, ctypes.POINTER(_Params), vp, vp]
         L.gc_gaussian.argtypes = [vp, i, i, i, f, i, vp, vp]
         L.gc_bilateral_direct.argtypes = [vp, i, i, i, f, f, vp, vp]
@@ -97,7 +99,7 @@ def _lib():
                      "gc_filter_host", "gc_filter_window", "gc_band_plan", "gc_comm_unique_id",
                      "gc_comm_init", "gc_comm_destroy", "gc_bilateral_band", "gc_gaussian", "gc_operator_taps",
                      "gc_bilateral_direct", "gc_band_exchange_plan", "gc_comm_wait", "gc_filter_band",
-                     "gc_scratch_trim", "gc_debug_oob_count", "gc_debug_oob_selftest"]:
+                     "gc_scratch_trim", "gc_debug_oob_count", "gc_debug_oob_selftest", "gc_filter_kernels"]:
             getattr(L, name).restype = ctypes.c_int
         _LIB = L
     return _LIB
@@ -214,6 +216,16 @@ def filter(img, sigma_s, sigma_r, N, c=None, L=0.0, U=255.0, out=None, op=OP_AUT
                "gc_filter")
     del keep
     return out
+
+
+def filter_kernels(B, H, W, sigma_s, sigma_r, N, c=None, L=0.0, U=255.0, op=OP_AUTO, fp64=False):
+    """gc_filter_kernels: kernels gc_filter launches for this shape and these parameters (1 = the
+    fused small-image FIR kernel, 2 = the two passes).  Host only."""
+    p, keep = _params(N, sigma_s, sigma_r, L, U, c, op, None, None, fp64)
+    n = ctypes.c_int(0)
+    _check(_lib().gc_filter_kernels(int(B), int(H), int(W), ctypes.byref(p), ctypes.byref(n)), "gc_filter_kernels")
+    del keep
+    return int(n.value)
 
 
 def gaussian(img, sigma_s, op=OP_AUTO, out=None, stream=None):

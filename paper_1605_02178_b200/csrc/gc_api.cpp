@@ -505,6 +505,23 @@ gc_status gc_filter(const float* imgs, int B, int H, int W, const gc_params* p, 
   return run(k, taps_host, reinterpret_cast<cudaStream_t>(stream));
 }
 
+gc_status gc_filter_kernels(int B, int H, int W, const gc_params* p, int* n_kernels) {
+  gc_status st = validate_params(p);
+  if (st != GC_OK) return st;
+  if (!n_kernels || B < 1 || H < 1 || W < 1) return GC_EINVAL;
+  KParams k;
+  std::memset(&k, 0, sizeof(k));
+  std::vector<float2> taps_host;
+  st = fill_constants(p, k, taps_host);
+  if (st != GC_OK) return st;
+  k.H = H;
+  k.Wd = W;
+  k.B = B;
+  k.in_rows = k.out_rows = H;
+  *n_kernels = fused_fir_applies(k) ? 1 : 2;
+  return GC_OK;
+}
+
 gc_status gc_gaussian(const float* imgs, int B, int H, int W, float sigma_s, int op, float* outs, void* stream) {
   gc_params p;
   gc_params_init(&p, 0, sigma_s, 1000.f);   // N = 0, one plane pair (f, 0); sigma_r unused

@@ -627,6 +627,7 @@ cudaError_t launch_rt(const KParams& p, cudaStream_t s) {
 }  // namespace
 
 cudaError_t launch_fir_two_pass(const KParams& p, cudaStream_t stream) {
+  if (fused_fir_applies(p)) return launch_fused_fir(p, stream);
   if (p.R >= 1 && p.R <= kMaxTemplW) return Table<kMaxTemplW>::go(p, stream);
   return launch_rt(p, stream);
 }

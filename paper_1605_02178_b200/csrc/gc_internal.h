@@ -179,6 +179,11 @@ cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
 // Launch the two-pass FIR pipeline (row pass + column pass with recombination) on
 // `stream`.  Scratch (the plane buffer) must already be in p.planes.
 cudaError_t launch_fir_two_pass(const KParams& p, cudaStream_t stream);
+// Small-image FIR path (gc_fused.cu): one launch, both passes of eq. (7) in shared memory per tile
+constexpr int kFuMaxW = kMaxTemplW;
+constexpr long long kFuMaxPx = GC_FUSED_MAX_PX;  // output pixels per call (B x rows x width)
+bool fused_fir_applies(const KParams& p);
+cudaError_t launch_fused_fir(const KParams& p, cudaStream_t stream);
 
 // Launch the two-pass O(1) exact-window pipeline (gc_o1.cu).  Same buffers and semantics.
 cudaError_t launch_o1_two_pass(const KParams& p, cudaStream_t stream);

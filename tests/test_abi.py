@@ -201,3 +201,24 @@ def test_operator_taps(gc, sigma_s):
     assert np.allclose(o1, o1[::-1], rtol=0, atol=1e-15)            # symmetric (cosines)
     auto = gc.operator_taps(sigma_s, gc.OP_AUTO)
     assert np.array_equal(auto, o1 if W >= 25 else fir)
+
+
+def test_filter_kernels(gc):
+    """gc_filter_kernels (host only): the small-image fused FIR kernel (1 launch) takes FIR calls
+    with W_s <= 24 and at most GC_FUSED_MAX_PX = 2^18 output pixels; everything else is 2 passes."""
+    if os.environ.get("GC_FIR_FUSED") is not None:
+        pytest.skip("GC_FIR_FUSED overrides the dispatch")
+    assert gc.filter_kernels(1, 256, 256, 3.0, 40.0, 5) == 1                 # c1: AUTO -> FIR, fused
+    assert gc.filter_kernels(1, 512, 512, 5.0, 40.0, 8) == 1                 # 2^18 pixels: still fused
+    assert gc.filter_kernels(1, 513, 512, 5.0, 40.0, 8) == 2
+    assert gc.filter_kernels(1, 1024, 1024, 5.0, 40.0, 8) == 2               # c2: two passes
+    assert gc.filter_kernels(4, 256, 256, 4.0, 40.0, 6) == 1                 # batch counts all images
+    assert gc.filter_kernels(5, 256, 256, 4.0, 40.0, 6) == 2
+    assert gc.filter_kernels(1, 64, 64, 9.0, 40.0, 5) == 2                   # W = 27: O(1) under AUTO
+    assert gc.filter_kernels(1, 64, 64, 9.0, 40.0, 5, op=gc.OP_FIR) == 2     # FIR above W = 24: runtime-W
+    assert gc.filter_kernels(1, 64, 64, 3.0, 40.0, 5, op=gc.OP_O1) == 2
+    assert gc.filter_kernels(1, 64, 64, 3.0, 40.0, 5, fp64=True) == 2
+    with pytest.raises(gc.GCError):
+        gc.filter_kernels(0, 64, 64, 3.0, 40.0, 5)
+    with pytest.raises(gc.GCError):
+        gc.filter_kernels(1, 64, 64, -1.0, 40.0, 5)

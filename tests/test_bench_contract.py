@@ -73,6 +73,15 @@ def test_roofline_fields():
     assert 0 < r["step_frac"] < r["frac"] * 2 and "derived" in r["peak_source"]
 
 
+def test_roofline_fused_kernel():
+    """The small-image FIR path is one kernel (empty "column" interval): its roofline counts the
+    whole step's algorithmic instructions against that kernel's time."""
+    px = 1024 * 1024
+    r = bench.roofline(8, 15, 1, px, row_ms=0.02, col_ms=0.003, step_ms=0.025, fused=True)
+    assert r["kernel"] == "k_fused_fir" and r["alg_instr_per_px"] == bench.alg_instr(8)["total"]
+    assert abs(r["achieved"] - bench.alg_instr(8)["total"] * px / 2e-5 / 1e12) < 1e-9
+
+
 @pytest.mark.parametrize("ws", [1, 2, 8])
 def test_check_rows_cover_every_seam(ws):
     """The untimed oracle check includes, for every band seam b, rows b-W, b-1, b and b+W-1."""

@@ -694,11 +694,15 @@ constexpr int kRPS = 4;          // image rows per ring stage: one [4 NP x 32] T
 
 // Shared memory: this head, then the ring of nst stages, each = kRPS entering rows followed by
 // kRPS leaving rows, a row = [NP pairs x 32 columns] float2.
+#ifndef GC_COLP_TILES
+#define GC_COLP_TILES 2
+#endif
+constexpr int kColT = GC_COLP_TILES;   // fold tile buffers: a warp runs up to kColT - 1 blocks ahead
 template <int NP>
 struct alignas(1024) ColPSmem {
   unsigned long long full[kPDMax], empty[kPDMax];
-  unsigned long long tile_full[2], tile_free[2];   // per tile buffer: all NP warps wrote / folded it
-  float2 tile[2][NP][NP][32];    // [buffer][row in block][pair][column]; a fold block = NP rows
+  unsigned long long tile_full[kColT], tile_free[kColT];   // per tile buffer: all NP warps wrote / folded it
+  float2 tile[kColT][NP][NP][32];    // [buffer][row in block][pair][column]; a fold block = NP rows
 };
 template <int NP>
 __host__ __device__ constexpr size_t colp_head() { return (sizeof(ColPSmem<NP>) + 1023) / 1024 * 1024; }
@@ -796,7 +800,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
       o1_mbar_init_n(&sm.full[st], 1);
       o1_mbar_init_n(&sm.empty[st], NP);
     }
-    for (int t = 0; t < 2; t++) {
+    for (int t = 0; t < kColT; t++) {
       o1_mbar_init_n(&sm.tile_full[t], NP);
       o1_mbar_init_n(&sm.tile_free[t], NP);
     }
@@ -915,9 +919,9 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
       fo = __ldg(row_ptr(p, b, p.out_row0 + pbs + q) + xc);
     }
     if (blk < nblk) {                               // ---- filter block blk into tile buffer blk & 1
-      const unsigned buf = blk & 1;
+      const unsigned buf = blk % kColT;
       const int nb = min(NP, ye - bs);
-      if (blk >= 2) mbar_wait_u32(tr0 + 8 * buf, ((blk >> 1) - 1) & 1);   // block blk-2 folded
+      if (blk >= kColT) mbar_wait_u32(tr0 + 8 * buf, ((blk / kColT) - 1) & 1);   // block blk-kColT folded
       float2* const tb = my_tile + buf * (NP * BOXF);
       auto step = [&](int jj) {
         if (r == 0) acquire();
@@ -940,8 +944,8 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
       if (lane == 0) o1_mbar_arrive(&sm.tile_full[buf]);
     }
     if (pb >= 0) {                                  // ---- fold row q of block pb: eqs. (8)-(10)
-      const unsigned pbuf = pb & 1;
-      mbar_wait_u32(tf0 + 8 * pbuf, (pb >> 1) & 1);   // every warp's pair of block pb is in
+      const unsigned pbuf = pb % kColT;
+      mbar_wait_u32(tf0 + 8 * pbuf, (pb / kColT) & 1);   // every warp's pair of block pb is in
       if (q < pnb) {
         const float a = p.raw ? 0.f : centre_a(p, fo);
         const float a2 = a * a;
@@ -1064,7 +1068,7 @@ cudaError_t launch_colp(const KParams& p0, cudaStream_t s) {
   const size_t cap = std::min<size_t>((size_t)(smem_sm > 0 ? smem_sm : 233472) / ctas - 1024, 227 * 1024);
   int nst = (int)((cap - colp_head<NP>()) / colp_stage<NP>());
   if (const char* env = std::getenv("GC_O1P_STAGES")) nst = std::min(nst, std::atoi(env));
-  nst = std::max((NP + kRPS - 1) / kRPS + 1, std::min(nst, kPDMax));   // (> one fold block: no starvation)
+  nst = std::max(kColT > 2 ? 2 : (NP + kRPS - 1) / kRPS + 1, std::min(nst, kPDMax));   // (> one fold block: no starvation)
   const size_t smem = colp_head<NP>() + (size_t)nst * colp_stage<NP>();
   static std::atomic<unsigned long long> ready{0};   // opt in to the largest ring once per device
   const cudaError_t e = once_per_device(ready, [&]() {

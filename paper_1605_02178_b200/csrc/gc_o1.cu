@@ -698,11 +698,18 @@ constexpr int kRPS = 4;          // image rows per ring stage: one [4 NP x 32] T
 #define GC_COLP_TILES 2
 #endif
 constexpr int kColT = GC_COLP_TILES;   // fold tile buffers: a warp runs up to kColT - 1 blocks ahead
+#ifndef GC_COLP_STAGE_BLOCKS
+#define GC_COLP_STAGE_BLOCKS 1
+#endif
+// rows per fold block: one ring stage (kRPS rows, the fold rotating over the warps), or NP rows
+// (every warp folds one row of every block; the stage position is then a runtime counter)
+template <int NP>
+constexpr int colp_block_rows() { return GC_COLP_STAGE_BLOCKS ? kRPS : NP; }
 template <int NP>
 struct alignas(1024) ColPSmem {
   unsigned long long full[kPDMax], empty[kPDMax];
   unsigned long long tile_full[kColT], tile_free[kColT];   // per tile buffer: all NP warps wrote / folded it
-  float2 tile[kColT][NP][NP][32];    // [buffer][row in block][pair][column]; a fold block = NP rows
+  float2 tile[kColT][colp_block_rows<NP>()][NP][32];       // [buffer][row in block][pair][column]
 };
 template <int NP>
 __host__ __device__ constexpr size_t colp_head() { return (sizeof(ColPSmem<NP>) + 1023) / 1024 * 1024; }
@@ -901,10 +908,102 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
   unsigned nguard = 0;
   const unsigned long long pol_out = l2_evict_first();
   const unsigned tf0 = smem_u32(&sm.tile_full[0]), tr0 = smem_u32(&sm.tile_free[0]);
-  // Blocks of NP output rows: block blk is filtered into tile buffer blk & 1 while block blk-1 is
-  // folded (eqs. 8-10) from the other buffer, warp q folding row q — every warp does the same work
-  // per block.  The mbarriers tile_full / tile_free give each warp a block of slack.  (Ring stages
-  // hold kRPS rows, so the stage position r is a runtime counter here.)
+  // Eqs. (8)-(10) for output row `row` from tile row `trow` of buffer `pbuf` (all NP pairs).
+  auto fold = [&](unsigned pbuf, int trow, int row, float fo) {
+    const float a = p.raw ? 0.f : centre_a(p, fo);
+    const float a2 = a * a;
+    float2 Q2 = make_float2(0.f, 0.f), P2 = Q2, pw2 = make_float2(1.f, a);
+    float vprev = 0.f, out_raw = 0.f;
+    const float2* const rt = &sm.tile[pbuf][trow][0][lane];
+#pragma unroll
+    for (int qq = 0; qq < NP; qq++) {
+      const float2 y = rt[qq * 32];
+      if (qq == 0) out_raw = y.x;
+      const float2 v = f2mul(p.chat2[qq], pw2);
+      Q2 = f2fma(v, y, Q2);
+      P2 = f2fma(make_float2(vprev, v.x), y, P2);
+      vprev = v.y;
+      pw2 = f2mul(pw2, f2s(a2));
+    }
+    const float Q = Q2.x + Q2.y, P = P2.x + P2.y;
+    if (xok) {
+      float o;
+      if (p.raw) {
+        o = out_raw;
+      } else if (Q > 0.f && isfinite(Q) && isfinite(P)) {
+        o = p.t_c + p.t_h * __fdividef(P, Q);          // eq. (10) + uncentring
+      } else {                                         // guard (R8)
+        o = fminf(fmaxf(fo, p.L), p.U);
+        nguard++;
+      }
+      GC_CHK(p, &outp[(long long)row * p.Wd], 4);
+      st_f_hint(&outp[(long long)row * p.Wd], o, pol_out);
+    }
+  };
+#if GC_COLP_STAGE_BLOCKS
+  // Blocks of kRPS output rows = one ring stage each (the lead-in ended on a stage boundary):
+  // block blk is filtered into tile buffer blk % kColT while block blk-1 is folded from its
+  // buffer; row j of block k is folded by warp (kRPS k + j) mod NP, so over NP blocks every warp
+  // folds kRPS rows.  tile_full / tile_free give each warp kColT - 1 blocks of slack.
+  constexpr int BR = kRPS;
+  const int nblk = (ye - ys + BR - 1) / BR;
+  float fo = 0.f;                                   // f at the row this warp folds next
+#pragma unroll 1
+  for (int blk = 0; blk <= nblk; blk++) {
+    const int bs = ys + blk * BR;
+    const int pb = blk - 1;                         // block folded in this iteration
+    const int pbs = bs - BR;
+    // rows of block pb this warp folds: fj, fj + NP, ... below pnb (more than one when NP < kRPS)
+    const int pnb = pb >= 0 ? min(BR, ye - pbs) : 0;
+    const int fj = pb >= 0 ? (q + NP - (BR * pb) % NP) % NP : BR;
+    if (fj < pnb) {                                 // used after the filtering
+      GC_CHK(p, row_ptr(p, b, p.out_row0 + pbs + fj) + xc, 4);
+      fo = __ldg(row_ptr(p, b, p.out_row0 + pbs + fj) + xc);
+    }
+    if (blk < nblk) {                               // ---- filter block blk into tile buffer blk % kColT
+      const unsigned buf = blk % kColT;
+      const int nb = min(BR, ye - bs);
+      if (blk >= kColT) mbar_wait_u32(tr0 + 8 * buf, ((blk / kColT) - 1) & 1);   // block blk-kColT folded
+      float2* const tb = my_tile + buf * (BR * BOXF);
+      acquire();
+      if (nb == BR) {
+#pragma unroll
+        for (int r = 0; r < BR; r++) {
+          const float2 pe = sbase[r * BOXF], pl = sbase[DIRF + r * BOXF];
+          tb[r * BOXF] = o1_output(p, S0, S);       // filtered pair q at row bs + r
+          advance(pe, pl);
+        }
+      } else {
+#pragma unroll 1
+        for (int r = 0; r < nb; r++) {
+          const float2 pe = sbase[r * BOXF], pl = sbase[DIRF + r * BOXF];
+          tb[r * BOXF] = o1_output(p, S0, S);
+          advance(pe, pl);
+        }
+      }
+      release();
+      __syncwarp();
+      if (lane == 0) o1_mbar_arrive(&sm.tile_full[buf]);
+    }
+    if (pb >= 0) {                                  // ---- fold row fj of block pb: eqs. (8)-(10)
+      const unsigned pbuf = pb % kColT;
+      mbar_wait_u32(tf0 + 8 * pbuf, (pb / kColT) & 1);   // every warp's pair of block pb is in
+      for (int j = fj; j < pnb; j += NP) {
+        if (j != fj) {
+          GC_CHK(p, row_ptr(p, b, p.out_row0 + pbs + j) + xc, 4);
+          fo = __ldg(row_ptr(p, b, p.out_row0 + pbs + j) + xc);
+        }
+        fold(pbuf, j, pbs + j, fo);
+      }
+      __syncwarp();
+      if (lane == 0) o1_mbar_arrive(&sm.tile_free[pbuf]);
+    }
+  }
+#else
+  // Blocks of NP output rows: block blk is filtered into tile buffer blk % kColT while block blk-1
+  // is folded (eqs. 8-10) from its buffer, warp q folding row q — every warp does the same work
+  // per block.  The mbarriers tile_full / tile_free give each warp kColT - 1 blocks of slack.
+  // (Ring stages hold kRPS rows, so the stage position r is a runtime counter here.)
   const int nblk = (ye - ys + NP - 1) / NP;
   int r = 0;                                        // row within the current ring stage
   float fo = 0.f;                                   // f at the row this warp folds next
@@ -918,7 +1017,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
       GC_CHK(p, row_ptr(p, b, p.out_row0 + pbs + q) + xc, 4);
       fo = __ldg(row_ptr(p, b, p.out_row0 + pbs + q) + xc);
     }
-    if (blk < nblk) {                               // ---- filter block blk into tile buffer blk & 1
+    if (blk < nblk) {                               // ---- filter block blk into tile buffer blk % kColT
       const unsigned buf = blk % kColT;
       const int nb = min(NP, ye - bs);
       if (blk >= kColT) mbar_wait_u32(tr0 + 8 * buf, ((blk / kColT) - 1) & 1);   // block blk-kColT folded
@@ -946,41 +1045,12 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
     if (pb >= 0) {                                  // ---- fold row q of block pb: eqs. (8)-(10)
       const unsigned pbuf = pb % kColT;
       mbar_wait_u32(tf0 + 8 * pbuf, (pb / kColT) & 1);   // every warp's pair of block pb is in
-      if (q < pnb) {
-        const float a = p.raw ? 0.f : centre_a(p, fo);
-        const float a2 = a * a;
-        float2 Q2 = make_float2(0.f, 0.f), P2 = Q2, pw2 = make_float2(1.f, a);
-        float vprev = 0.f, out_raw = 0.f;
-        const float2* const rt = &sm.tile[pbuf][q][0][lane];
-#pragma unroll
-        for (int qq = 0; qq < NP; qq++) {
-          const float2 y = rt[qq * 32];
-          if (qq == 0) out_raw = y.x;
-          const float2 v = f2mul(p.chat2[qq], pw2);
-          Q2 = f2fma(v, y, Q2);
-          P2 = f2fma(make_float2(vprev, v.x), y, P2);
-          vprev = v.y;
-          pw2 = f2mul(pw2, f2s(a2));
-        }
-        const float Q = Q2.x + Q2.y, P = P2.x + P2.y;
-        if (xok) {
-          float o;
-          if (p.raw) {
-            o = out_raw;
-          } else if (Q > 0.f && isfinite(Q) && isfinite(P)) {
-            o = p.t_c + p.t_h * __fdividef(P, Q);          // eq. (10) + uncentring
-          } else {                                         // guard (R8)
-            o = fminf(fmaxf(fo, p.L), p.U);
-            nguard++;
-          }
-          GC_CHK(p, &outp[(long long)(pbs + q) * p.Wd], 4);
-          st_f_hint(&outp[(long long)(pbs + q) * p.Wd], o, pol_out);
-        }
-      }
+      if (q < pnb) fold(pbuf, q, pbs + q, fo);
       __syncwarp();
       if (lane == 0) o1_mbar_arrive(&sm.tile_free[pbuf]);
     }
   }
+#endif
   count_guarded(p.fallback, 0xffffffffu, nguard);
 }
 
@@ -1068,7 +1138,9 @@ cudaError_t launch_colp(const KParams& p0, cudaStream_t s) {
   const size_t cap = std::min<size_t>((size_t)(smem_sm > 0 ? smem_sm : 233472) / ctas - 1024, 227 * 1024);
   int nst = (int)((cap - colp_head<NP>()) / colp_stage<NP>());
   if (const char* env = std::getenv("GC_O1P_STAGES")) nst = std::min(nst, std::atoi(env));
-  nst = std::max(kColT > 2 ? 2 : (NP + kRPS - 1) / kRPS + 1, std::min(nst, kPDMax));   // (> one fold block: no starvation)
+  // (more than one fold block of rows in the ring: no starvation)
+  const int min_st = (colp_block_rows<NP>() + kRPS - 1) / kRPS + (kColT > 2 ? 0 : 1);
+  nst = std::max(std::max(2, min_st), std::min(nst, kPDMax));
   const size_t smem = colp_head<NP>() + (size_t)nst * colp_stage<NP>();
   static std::atomic<unsigned long long> ready{0};   // opt in to the largest ring once per device
   const cudaError_t e = once_per_device(ready, [&]() {

@@ -695,7 +695,7 @@ constexpr int kRPS = 4;          // image rows per ring stage: one [4 NP x 32] T
 // Shared memory: this head, then the ring of nst stages, each = kRPS entering rows followed by
 // kRPS leaving rows, a row = [NP pairs x 32 columns] float2.
 #ifndef GC_COLP_TILES
-#define GC_COLP_TILES 2
+#define GC_COLP_TILES 3
 #endif
 constexpr int kColT = GC_COLP_TILES;   // fold tile buffers: a warp runs up to kColT - 1 blocks ahead
 #ifndef GC_COLP_STAGE_BLOCKS
@@ -740,6 +740,9 @@ __device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned phase) {
       "r"(phase)
       : "memory");
 }
+#ifndef GC_COLP_BACKOFF_NS
+#define GC_COLP_BACKOFF_NS 128
+#endif
 __device__ __forceinline__ void mbar_wait_backoff(unsigned bar, unsigned phase) {
   for (;;) {
     unsigned ok;
@@ -753,7 +756,7 @@ __device__ __forceinline__ void mbar_wait_backoff(unsigned bar, unsigned phase) 
         : "r"(bar), "r"(phase)
         : "memory");
     if (ok) return;
-    __nanosleep(128);
+    __nanosleep(GC_COLP_BACKOFF_NS);
   }
 }
 __device__ __forceinline__ float2 lds64(unsigned a) {
@@ -909,7 +912,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
   const unsigned long long pol_out = l2_evict_first();
   const unsigned tf0 = smem_u32(&sm.tile_full[0]), tr0 = smem_u32(&sm.tile_free[0]);
   // Eqs. (8)-(10) for output row `row` from tile row `trow` of buffer `pbuf` (all NP pairs).
-  auto fold = [&](unsigned pbuf, int trow, int row, float fo) {
+  auto fold = [&](unsigned pbuf, int trow, float* orow, float fo) {   // orow: output row, column x
     const float a = p.raw ? 0.f : centre_a(p, fo);
     const float a2 = a * a;
     float2 Q2 = make_float2(0.f, 0.f), P2 = Q2, pw2 = make_float2(1.f, a);
@@ -936,8 +939,8 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
         o = fminf(fmaxf(fo, p.L), p.U);
         nguard++;
       }
-      GC_CHK(p, &outp[(long long)row * p.Wd], 4);
-      st_f_hint(&outp[(long long)row * p.Wd], o, pol_out);
+      GC_CHK(p, orow, 4);
+      st_f_hint(orow, o, pol_out);
     }
   };
 #if GC_COLP_STAGE_BLOCKS
@@ -946,24 +949,42 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
   // buffer; row j of block k is folded by warp (kRPS k + j) mod NP, so over NP blocks every warp
   // folds kRPS rows.  tile_full / tile_free give each warp kColT - 1 blocks of slack.
   constexpr int BR = kRPS;
-  const int nblk = (ye - ys + BR - 1) / BR;
+  const int nrows = ye - ys;
+  const int nblk = (nrows + BR - 1) / BR;
+  // Row j of block k is folded by warp (kRPS k + j) mod NP, i.e. warp q folds the rows ys + q,
+  // ys + q + NP, ... — tracked as a running offset and running f / output pointers instead of
+  // per-block index arithmetic (the block loop's integer work was a third of its instructions).
+  const float* const frun = row_run_ptr(p, b, p.out_row0 + ys, nrows);   // null if the strip spans segments
+  int nr = q;                                       // offset (from ys) of the next row this warp folds
+  const long long fstep = (long long)NP * p.Wd;
+  const float* fpn = frun ? frun + (long long)q * p.Wd + xc : nullptr;
+  float* opn = outp + (long long)(ys + q) * p.Wd;
+  auto fload = [&]() -> float {
+    if (fpn) {
+      GC_CHK(p, fpn, 4);
+      return __ldg(fpn);
+    }
+    GC_CHK(p, row_ptr(p, b, p.out_row0 + ys + nr) + xc, 4);
+    return __ldg(row_ptr(p, b, p.out_row0 + ys + nr) + xc);
+  };
   float fo = 0.f;                                   // f at the row this warp folds next
 #pragma unroll 1
   for (int blk = 0; blk <= nblk; blk++) {
-    const int bs = ys + blk * BR;
     const int pb = blk - 1;                         // block folded in this iteration
-    const int pbs = bs - BR;
-    // rows of block pb this warp folds: fj, fj + NP, ... below pnb (more than one when NP < kRPS)
-    const int pnb = pb >= 0 ? min(BR, ye - pbs) : 0;
-    const int fj = pb >= 0 ? (q + NP - (BR * pb) % NP) % NP : BR;
-    if (fj < pnb) {                                 // used after the filtering
-      GC_CHK(p, row_ptr(p, b, p.out_row0 + pbs + fj) + xc, 4);
-      fo = __ldg(row_ptr(p, b, p.out_row0 + pbs + fj) + xc);
-    }
+    const int pend = min(BR * blk, nrows);          // rows [0, pend) are filtered after this iteration
+    const bool folds = nr < pend;                   // this warp folds a row of block pb
+    if (folds) fo = fload();                        // used after the filtering
     if (blk < nblk) {                               // ---- filter block blk into tile buffer blk % kColT
+      const int bs = ys + blk * BR;
       const unsigned buf = blk % kColT;
       const int nb = min(BR, ye - bs);
-      if (blk >= kColT) mbar_wait_u32(tr0 + 8 * buf, ((blk / kColT) - 1) & 1);   // block blk-kColT folded
+#ifndef GC_COLP_TF_BACKOFF
+#define GC_COLP_TF_BACKOFF 0
+#endif
+      if (blk >= kColT) {                           // block blk-kColT folded
+        if (GC_COLP_TF_BACKOFF) mbar_wait_backoff(tr0 + 8 * buf, ((blk / kColT) - 1) & 1);
+        else mbar_wait_u32(tr0 + 8 * buf, ((blk / kColT) - 1) & 1);
+      }
       float2* const tb = my_tile + buf * (BR * BOXF);
       acquire();
       if (nb == BR) {
@@ -985,16 +1006,24 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
       __syncwarp();
       if (lane == 0) o1_mbar_arrive(&sm.tile_full[buf]);
     }
-    if (pb >= 0) {                                  // ---- fold row fj of block pb: eqs. (8)-(10)
+    if (pb >= 0) {                                  // ---- fold this warp's rows of block pb: eqs. (8)-(10)
       const unsigned pbuf = pb % kColT;
-      mbar_wait_u32(tf0 + 8 * pbuf, (pb / kColT) & 1);   // every warp's pair of block pb is in
-      for (int j = fj; j < pnb; j += NP) {
-        if (j != fj) {
-          GC_CHK(p, row_ptr(p, b, p.out_row0 + pbs + j) + xc, 4);
-          fo = __ldg(row_ptr(p, b, p.out_row0 + pbs + j) + xc);
+#ifndef GC_COLP_SKIP_FULL_WAIT
+#define GC_COLP_SKIP_FULL_WAIT 1
+#endif
+      if (!GC_COLP_SKIP_FULL_WAIT && !folds) mbar_wait_u32(tf0 + 8 * pbuf, (pb / kColT) & 1);
+      if (folds) {
+        mbar_wait_u32(tf0 + 8 * pbuf, (pb / kColT) & 1);   // every warp's pair of block pb is in
+        for (bool first = true; nr < pend; first = false) {   // (more than one row when NP < kRPS)
+          if (!first) fo = fload();
+          fold(pbuf, nr - BR * pb, opn, fo);
+          nr += NP;
+          if (fpn) fpn += fstep;
+          opn += fstep;
         }
-        fold(pbuf, j, pbs + j, fo);
       }
+      // (a warp folding nothing here may free the buffer at once: a warp reaching block pb + kColT
+      // first waits for this phase, so no arrival can count towards a later one)
       __syncwarp();
       if (lane == 0) o1_mbar_arrive(&sm.tile_free[pbuf]);
     }
@@ -1045,7 +1074,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
     if (pb >= 0) {                                  // ---- fold row q of block pb: eqs. (8)-(10)
       const unsigned pbuf = pb % kColT;
       mbar_wait_u32(tf0 + 8 * pbuf, (pb / kColT) & 1);   // every warp's pair of block pb is in
-      if (q < pnb) fold(pbuf, q, pbs + q, fo);
+      if (q < pnb) fold(pbuf, q, outp + (long long)(pbs + q) * p.Wd, fo);
       __syncwarp();
       if (lane == 0) o1_mbar_arrive(&sm.tile_free[pbuf]);
     }

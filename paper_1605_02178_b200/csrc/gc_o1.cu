@@ -724,6 +724,9 @@ __device__ __forceinline__ void o1_mbar_arrive(unsigned long long* bar) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s) : "memory");
 }
+__device__ __forceinline__ void o1_mbar_arrive_u32(unsigned s) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s) : "memory");
+}
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
@@ -880,18 +883,26 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
   int st = 0;
   unsigned ph = 0;
   const float2* sbase = my_ring;                    // this lane's sample in the current stage
+  // shared address of the barrier block (full[], empty[], tile_full[], tile_free[] are contiguous),
+  // kept in a register: recomputed from the shared window base (S2R SR_CgaCtaId) at every use it
+  // was a visible stall site of the block loop (ncu r02bc)
+  unsigned bar0;
+  asm volatile("mov.b32 %0, %1;" : "=r"(bar0) : "r"(smem_u32(&sm.full[0])));
+  static_assert(offsetof(ColPSmem<NP>, empty) == 8 * kPDMax && offsetof(ColPSmem<NP>, tile_full) == 16 * kPDMax &&
+                    offsetof(ColPSmem<NP>, tile_free) == 16 * kPDMax + 8 * kColT,
+                "ColPSmem barrier block layout");
   auto advance = [&](float2 pe, float2 pl) {        // window i -> i+1
     o1_update(p, S0, S, D, f2add(pe, Lp), f2add(Ep, pl), pe, pl);
     Ep = pe;
     Lp = pl;
   };
   auto acquire = [&]() {
-    mbar_wait_u32(smem_u32(&sm.full[st]), ph);
+    mbar_wait_u32(bar0 + 8 * st, ph);
     sbase = my_ring + st * SBF;
   };
   auto release = [&]() {
     __syncwarp();
-    if (lane == 0) o1_mbar_arrive(&sm.empty[st]);
+    if (lane == 0) o1_mbar_arrive_u32(bar0 + 8 * (kPDMax + st));
     if (++st == nst) { st = 0; ph ^= 1; }
   };
   // lead-in: whole stages, no output; leaving samples real from step zl on.  (The direct lead-in
@@ -910,7 +921,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
   float* const outp = p.out + b * p.out_img_stride + x;
   unsigned nguard = 0;
   const unsigned long long pol_out = l2_evict_first();
-  const unsigned tf0 = smem_u32(&sm.tile_full[0]), tr0 = smem_u32(&sm.tile_free[0]);
+  const unsigned tf0 = bar0 + 16 * kPDMax, tr0 = tf0 + 8 * kColT;
   // Eqs. (8)-(10) for output row `row` from tile row `trow` of buffer `pbuf` (all NP pairs).
   auto fold = [&](unsigned pbuf, int trow, float* orow, float fo) {   // orow: output row, column x
     const float a = p.raw ? 0.f : centre_a(p, fo);
@@ -968,23 +979,26 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
     return __ldg(row_ptr(p, b, p.out_row0 + ys + nr) + xc);
   };
   float fo = 0.f;                                   // f at the row this warp folds next
+  // tile buffer of block blk / of block blk - 1 and their mbarrier phase parities (blk / kColT) & 1,
+  // (blk - 1) / kColT & 1 as rolling counters (a modulo by kColT = 3 was a visible stall site)
+  unsigned buf = 0, bph = 0, pbuf = 0, pph = 0;
+#ifndef GC_COLP_FOLD_LAG
+#define GC_COLP_FOLD_LAG 1
+#endif
+  // iteration blk filters block blk and folds block blk - FL: a folder may run FL - 1 blocks ahead
+  // of the slowest filtering warp, a filtering warp kColT - FL blocks ahead of the slowest folder
+  constexpr int FL = GC_COLP_FOLD_LAG;
+  static_assert(FL >= 1 && FL < kColT, "fold lag needs kColT > FL tile buffers");
 #pragma unroll 1
-  for (int blk = 0; blk <= nblk; blk++) {
-    const int pb = blk - 1;                         // block folded in this iteration
-    const int pend = min(BR * blk, nrows);          // rows [0, pend) are filtered after this iteration
+  for (int blk = 0; blk < nblk + FL; blk++) {
+    const int pb = blk - FL;                        // block folded in this iteration
+    const int pend = min(BR * (pb + 1), nrows);     // rows [0, pend) are in blocks <= pb
     const bool folds = nr < pend;                   // this warp folds a row of block pb
     if (folds) fo = fload();                        // used after the filtering
-    if (blk < nblk) {                               // ---- filter block blk into tile buffer blk % kColT
+    if (blk < nblk) {                               // ---- filter block blk into tile buffer buf
       const int bs = ys + blk * BR;
-      const unsigned buf = blk % kColT;
       const int nb = min(BR, ye - bs);
-#ifndef GC_COLP_TF_BACKOFF
-#define GC_COLP_TF_BACKOFF 0
-#endif
-      if (blk >= kColT) {                           // block blk-kColT folded
-        if (GC_COLP_TF_BACKOFF) mbar_wait_backoff(tr0 + 8 * buf, ((blk / kColT) - 1) & 1);
-        else mbar_wait_u32(tr0 + 8 * buf, ((blk / kColT) - 1) & 1);
-      }
+      if (blk >= kColT) mbar_wait_u32(tr0 + 8 * buf, bph ^ 1);   // block blk - kColT folded
       float2* const tb = my_tile + buf * (BR * BOXF);
       acquire();
       if (nb == BR) {
@@ -1004,16 +1018,11 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
       }
       release();
       __syncwarp();
-      if (lane == 0) o1_mbar_arrive(&sm.tile_full[buf]);
+      if (lane == 0) o1_mbar_arrive_u32(tf0 + 8 * buf);
     }
     if (pb >= 0) {                                  // ---- fold this warp's rows of block pb: eqs. (8)-(10)
-      const unsigned pbuf = pb % kColT;
-#ifndef GC_COLP_SKIP_FULL_WAIT
-#define GC_COLP_SKIP_FULL_WAIT 1
-#endif
-      if (!GC_COLP_SKIP_FULL_WAIT && !folds) mbar_wait_u32(tf0 + 8 * pbuf, (pb / kColT) & 1);
       if (folds) {
-        mbar_wait_u32(tf0 + 8 * pbuf, (pb / kColT) & 1);   // every warp's pair of block pb is in
+        mbar_wait_u32(tf0 + 8 * pbuf, pph);         // every warp's pair of block pb is in
         for (bool first = true; nr < pend; first = false) {   // (more than one row when NP < kRPS)
           if (!first) fo = fload();
           fold(pbuf, nr - BR * pb, opn, fo);
@@ -1022,10 +1031,18 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
           opn += fstep;
         }
       }
-      // (a warp folding nothing here may free the buffer at once: a warp reaching block pb + kColT
+      // (a warp folding nothing here frees the buffer at once: a warp reaching block pb + kColT
       // first waits for this phase, so no arrival can count towards a later one)
       __syncwarp();
-      if (lane == 0) o1_mbar_arrive(&sm.tile_free[pbuf]);
+      if (lane == 0) o1_mbar_arrive_u32(tr0 + 8 * pbuf);
+    }
+    if (pb >= 0 && ++pbuf == kColT) {
+      pbuf = 0;
+      pph ^= 1;
+    }
+    if (++buf == kColT) {
+      buf = 0;
+      bph ^= 1;
     }
   }
 #else
@@ -1069,14 +1086,14 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
         for (int jj = 0; jj < nb; jj++) step(jj);
       }
       __syncwarp();
-      if (lane == 0) o1_mbar_arrive(&sm.tile_full[buf]);
+      if (lane == 0) o1_mbar_arrive_u32(tf0 + 8 * buf);
     }
     if (pb >= 0) {                                  // ---- fold row q of block pb: eqs. (8)-(10)
       const unsigned pbuf = pb % kColT;
       mbar_wait_u32(tf0 + 8 * pbuf, (pb / kColT) & 1);   // every warp's pair of block pb is in
       if (q < pnb) fold(pbuf, q, outp + (long long)(pbs + q) * p.Wd, fo);
       __syncwarp();
-      if (lane == 0) o1_mbar_arrive(&sm.tile_free[pbuf]);
+      if (lane == 0) o1_mbar_arrive_u32(tr0 + 8 * pbuf);
     }
   }
 #endif

@@ -100,6 +100,29 @@ def _free_port():
     return p
 
 
+_JSON_FD = None
+
+
+def _quiet_stdout():
+    """Keep fd 1 for the one JSON line: anything native code writes to stdout (NCCL prints its
+    version banner there when NCCL_DEBUG asks for it) goes to stderr instead."""
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def _emit(line):
+    s = json.dumps(line) + "\n"
+    if _JSON_FD is None:
+        sys.stdout.write(s)
+        sys.stdout.flush()
+    else:
+        sys.stdout.flush()
+        os.write(_JSON_FD, s.encode())
+
+
 def _self_launch(n):
     """`--gpus N` outside torchrun: re-run this command under torchrun with N ranks."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
@@ -377,7 +400,7 @@ def run_reference(args, cfg, sigma_s, sigma_r, ws, rank):
             "cpu_baseline": {"value": v, "unit": "MP/s", "cores": co.cores, "kind": "oracle",
                              "sample": co.describe(co.cores, args.steps, t_tot) + " per timed step"},
             "e2e": {"value": v, "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    _emit(line)
 
 
 def band_rows_of(H, ws):
@@ -510,6 +533,7 @@ def main():
     ws, rank, local = _dist()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return _self_launch(args.gpus)
+    _quiet_stdout()
     from synth import CONFIGS, config_image
     cfg = CONFIGS[args.workload]
     sigma_s = args.sigma_s if args.sigma_s is not None else cfg.sigma_s[0]
@@ -755,7 +779,7 @@ def main():
         line["c3_sweep"] = c3_sweep(gc, dev, 10)
     if ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, sigma_s, sigma_r, cfg.N)
-    print(json.dumps(line), flush=True)
+    _emit(line)
 
 
 if __name__ == "__main__":

@@ -37,6 +37,18 @@ def test_reference_arm_json_line():
     assert d["e2e"] == {"value": d["value"], "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
 
 
+def test_json_line_alone_on_stdout():
+    """Native code writing to fd 1 (NCCL's version banner under NCCL_DEBUG=VERSION) must not reach
+    the driver's stdout: after _quiet_stdout only the JSON line does."""
+    code = ("import os, sys; sys.path.insert(0, %r); import bench; bench._quiet_stdout(); "
+            "os.write(1, b'NCCL version 0.0.0\\n'); print('python noise'); bench._emit({'metric': 'm', 'value': 1.0})"
+            % ROOT)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout == '{"metric": "m", "value": 1.0}\n'
+    assert "NCCL version" in r.stderr and "python noise" in r.stderr
+
+
 def test_flop_accounting():
     """FIR: 2(2R+1) FLOP per plane-pixel and pass; O(1): 37; Deriche: 35 (N+2 planes)."""
     N, R, px = 8, 15, 1000

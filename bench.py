@@ -182,7 +182,21 @@ def flops_col(N, R, px, op=1):
     return px * ((N + 2) * op_flop_per_plane(op, R) + 6 * (N + 1) + 8)
 
 
-def roofline(N, R, op, px, row_ms, col_ms, step_ms, traffic_key=None, fused=False):
+def _traffic(tr, key, kern, px, px_full):
+    """DRAM bytes of one launch of `kern` covering px pixels, from profiles/traffic.json (values
+    are per launch of the one-GPU workload: a rank's shard or row band takes its share)."""
+    base = key.rsplit("_g", 1)[0]
+    t = tr.get(f"{base}:{kern}")
+    if not t:
+        return None, None
+    src = tr.get("_source_" + base, tr.get("_source"))
+    if px_full and px != px_full:
+        t = t * px / px_full
+        src = "per pixel of %s, scaled to this rank's share (%s)" % (base, src)
+    return t, src
+
+
+def roofline(N, R, op, px, row_ms, col_ms, step_ms, traffic_key=None, fused=False, px_full=None):
     """Roofline of the dominant kernel: `achieved`/`frac` on SURVEY §8(d)'s
     algorithmic instruction count against the derived FP32 ALU peak; `design` = the same kernel's
     implemented FLOP against 74.45 TFLOP/s; `step_frac` = the whole step on the algorithmic count.
@@ -211,11 +225,11 @@ def roofline(N, R, op, px, row_ms, col_ms, step_ms, traffic_key=None, fused=Fals
     if traffic_key and os.path.exists(tp):
         try:
             tr = json.load(open(tp))
-            t = tr.get(f"{traffic_key}:{dom}")
+            t, src = _traffic(tr, traffic_key, dom, px, px_full)
             if t:
                 out["traffic"] = t
                 out["traffic_bytes_per_px"] = t / px
-                out["traffic_source"] = tr.get("_source_" + traffic_key, tr.get("_source"))
+                out["traffic_source"] = src
         except Exception:
             pass
     return out
@@ -736,7 +750,8 @@ def main():
     roof = kernels = None
     if row_ms is not None:
         key = f"{cfg.name}_s{sigma_s:g}_{ {1: 'fir', 2: 'o1', 3: 'deriche'}[op]}" + (f"_g{ws}" if comm else "")
-        roof = roofline(cfg.N, R, op, px_rank, row_ms, col_ms, ms_step, traffic_key=key, fused=fused)
+        roof = roofline(cfg.N, R, op, px_rank, row_ms, col_ms, ms_step, traffic_key=key, fused=fused,
+                        px_full=cfg.batch * cfg.H * cfg.W)
         fr, fc = flops_row(cfg.N, R, px_rank, op), flops_col(cfg.N, R, px_rank, op)
         if fused:
             kernels = {"k_fused_fir": {"ms": row_ms, "design_tflops": (fr + fc) / row_ms / 1e9}}
@@ -756,6 +771,26 @@ def main():
     hbm = {"algorithmic_bytes_per_px": 8, "achieved_GBps": 8 * px_rank / (ms_step / 1e3) / 1e9,
            "peak_GBps": HBM_PEAK_GBPS, "peak_source": HBM_PEAK_SOURCE}
     hbm["frac_of_measured"] = hbm["achieved_GBps"] / HBM_PEAK_GBPS
+    if row_ms is not None and not fused:
+        # the DRAM bytes the kernels actually move (ncu, profiles/traffic.json) over this run's kernel
+        # times: how close the implementation runs to the HBM roof, beside the algorithmic 8 B/px
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+            px_full = cfg.batch * cfg.H * cfg.W
+            tt = {k: _traffic(tr, key, k, px_rank, px_full) for k in ("k_row", "k_col")}
+            tb = {k: v[0] for k, v in tt.items()}
+            if all(tb.values()):
+                dm = {k: {"bytes_per_px": tb[k] / px_rank, "GBps": tb[k] / ms / 1e6,
+                          "frac_of_measured": tb[k] / ms / 1e6 / HBM_PEAK_GBPS}
+                      for k, ms in (("k_row", row_ms), ("k_col", col_ms))}
+                step_gbps = (tb["k_row"] + tb["k_col"]) / ms_step / 1e6
+                dm["step"] = {"bytes_per_px": (tb["k_row"] + tb["k_col"]) / px_rank, "GBps": step_gbps,
+                              "frac_of_measured": step_gbps / HBM_PEAK_GBPS}
+                dm["source"] = ("ncu dram bytes per launch (profiles/traffic.json: %s) / CUDA-event kernel times"
+                                % tt["k_col"][1])
+                hbm["dram_measured"] = dm
+        except Exception:
+            pass
     csum = clk.summary()
     energy = None
     if csum.get("power_w_median"):

@@ -128,3 +128,14 @@ def test_oracle_check_crop_is_exact():
     finally:
         synth.config_image = real
     assert chk["max_abs"] < 1e-4 and chk["pass"]
+
+
+def test_traffic_share_of_a_rank():
+    """traffic.json holds DRAM bytes per launch of the one-GPU workload: a rank's row band (key
+    suffix _g<N>) or batch shard takes its pixel share, so bytes per pixel do not change with N."""
+    tr = {"c5_s16_o1:k_col": 1000.0, "_source": "s"}
+    full = 100
+    t1, _ = bench._traffic(tr, "c5_s16_o1", "k_col", full, full)
+    t2, src = bench._traffic(tr, "c5_s16_o1_g4", "k_col", full // 4, full)
+    assert t1 == 1000.0 and t2 == 250.0 and "share" in src
+    assert bench._traffic(tr, "c5_s16_o1", "k_row", full, full) == (None, None)

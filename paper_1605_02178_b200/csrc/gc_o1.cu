@@ -786,11 +786,31 @@ __device__ __forceinline__ void tma_2d_hint(unsigned dst, const CUtensorMap* map
       : "memory");
 }
 
+// Dedicated fold warps: with F = colp_folders<NP>() > 0, warps NP+1 .. NP+F fold (warp NP+1+i
+// folds row i of every 4-row block) and the consumers only filter, instead of the consumers
+// folding in rotation.  Measured (r02bm): NP = 7 (c5) column pass -4 % at 3 CTAs/SM (12 warps,
+// 56 registers); NP = 6 (c3) +1.5 %, so the auto choice (GC_COLP_FOLDERS = -1) takes them for
+// NP = 7 only; 0 / 4 force them off / on.
+#ifndef GC_COLP_FOLDERS
+#define GC_COLP_FOLDERS -1
+#endif
+#ifndef GC_COLP_FOLD_CTAS
+#define GC_COLP_FOLD_CTAS 3
+#endif
 template <int NP>
-__global__ void __launch_bounds__(32 * (NP + 1), 3)
+__host__ __device__ constexpr int colp_folders() {
+  return GC_COLP_STAGE_BLOCKS ? (GC_COLP_FOLDERS >= 0 ? GC_COLP_FOLDERS : (NP == 7 ? kRPS : 0)) : 0;
+}
+template <int NP>
+__host__ __device__ constexpr int colp_ctas() { return colp_folders<NP>() ? GC_COLP_FOLD_CTAS : 3; }
+
+template <int NP>
+__global__ void __launch_bounds__(32 * (NP + 1 + colp_folders<NP>()), colp_ctas<NP>())
     k_col_o1p(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap4, const KParams p) {
   extern __shared__ __align__(1024) float4 smem_o1p[];
   ColPSmem<NP>& sm = *reinterpret_cast<ColPSmem<NP>*>(smem_o1p);
+  constexpr int kColF = colp_folders<NP>();
+  static_assert(kColF == 0 || kColF == kRPS, "fold warps: one per row of a stage block");
   constexpr unsigned BOX = NP * 32u * 8u;           // one image row: [NP pairs x 32 columns]
   constexpr unsigned DIR = kRPS * BOX;              // one direction of a stage (kRPS rows)
   constexpr unsigned SB = 2u * DIR;                 // stage: entering rows, then leaving rows
@@ -815,7 +835,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
     }
     for (int t = 0; t < kColT; t++) {
       o1_mbar_init_n(&sm.tile_full[t], NP);
-      o1_mbar_init_n(&sm.tile_free[t], NP);
+      o1_mbar_init_n(&sm.tile_free[t], kColF ? kColF : NP);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -907,8 +927,9 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
   };
   // lead-in: whole stages, no output; leaving samples real from step zl on.  (The direct lead-in
   // of the row pass measured no faster here, r02al: this loop waits on the TMA ring anyway.)
+  const bool filters = kColF == 0 || warp < NP;    // (fold warps skip the recursion)
 #pragma unroll 1
-  for (int k0 = 0; k0 < lead; k0 += kRPS) {
+  for (int k0 = 0; filters && k0 < lead; k0 += kRPS) {
     acquire();
 #pragma unroll
     for (int r = 0; r < kRPS; r++) {
@@ -955,6 +976,71 @@ __global__ void __launch_bounds__(32 * (NP + 1), 3)
     }
   };
 #if GC_COLP_STAGE_BLOCKS
+  if constexpr (kColF > 0) {
+    // Dedicated fold warps: consumers filter block blk into tile buffer blk % kColT (after its
+    // previous block was folded), fold warp fi folds row fi of every block.
+    const int nblk = (ye - ys + kRPS - 1) / kRPS;
+    unsigned buf = 0, bph = 0;
+    if (warp < NP) {
+#pragma unroll 1
+      for (int blk = 0; blk < nblk; blk++) {
+        const int bs = ys + blk * kRPS;
+        const int nb = min(kRPS, ye - bs);
+        if (blk >= kColT) mbar_wait_u32(tr0 + 8 * buf, bph ^ 1);   // block blk - kColT folded
+        float2* const tb = my_tile + buf * (kRPS * BOXF);
+        acquire();
+        if (nb == kRPS) {
+#pragma unroll
+          for (int r = 0; r < kRPS; r++) {
+            const float2 pe = sbase[r * BOXF], pl = sbase[DIRF + r * BOXF];
+            tb[r * BOXF] = o1_output(p, S0, S);
+            advance(pe, pl);
+          }
+        } else {
+#pragma unroll 1
+          for (int r = 0; r < nb; r++) {
+            const float2 pe = sbase[r * BOXF], pl = sbase[DIRF + r * BOXF];
+            tb[r * BOXF] = o1_output(p, S0, S);
+            advance(pe, pl);
+          }
+        }
+        release();
+        __syncwarp();
+        if (lane == 0) o1_mbar_arrive_u32(tf0 + 8 * buf);
+        if (++buf == kColT) {
+          buf = 0;
+          bph ^= 1;
+        }
+      }
+    } else {
+      const int fi = warp - NP - 1;                 // the row of every block this warp folds
+      auto frow = [&](int blk) -> float {           // f at row fi of block blk (0 past the strip)
+        const int r = ys + blk * kRPS + fi;
+        if (blk >= nblk || r >= ye) return 0.f;
+        GC_CHK(p, row_ptr(p, b, p.out_row0 + r) + xc, 4);
+        return __ldg(row_ptr(p, b, p.out_row0 + r) + xc);
+      };
+      float fo_next = frow(0);
+#pragma unroll 1
+      for (int blk = 0; blk < nblk; blk++) {
+        const int r = ys + blk * kRPS + fi;
+        const float fo = fo_next;
+        fo_next = frow(blk + 1);                    // one block ahead: this warp has the time
+        if (r < ye) {
+          mbar_wait_u32(tf0 + 8 * buf, bph);        // every consumer's pair of block blk is in
+          fold(buf, fi, outp + (long long)r * p.Wd, fo);
+        }
+        __syncwarp();
+        if (lane == 0) o1_mbar_arrive_u32(tr0 + 8 * buf);
+        if (++buf == kColT) {
+          buf = 0;
+          bph ^= 1;
+        }
+      }
+    }
+    count_guarded(p.fallback, 0xffffffffu, nguard);
+    return;
+  }
   // Blocks of kRPS output rows = one ring stage each (the lead-in ended on a stage boundary):
   // block blk is filtered into tile buffer blk % kColT while block blk-1 is folded from its
   // buffer; row j of block k is folded by warp (kRPS k + j) mod NP, so over NP blocks every warp
@@ -1158,13 +1244,13 @@ cudaError_t launch_col(const KParams& p0, cudaStream_t s) {
 
 // CTAs per SM for k_col_o1p: bounds the GPU's in-flight leaving-row windows (CTAs x 148 x
 // NP x 32 x (2W+1) x 8 B) so they stay L2-resident; GC_O1P_CTAS overrides (development A/B).
-int o1p_ctas_per_sm() {
+int o1p_ctas_per_sm(int dflt) {
   static const int v = [] {
     const char* e = std::getenv("GC_O1P_CTAS");
-    const int n = e ? std::atoi(e) : 3;
-    return n < 1 ? 1 : (n > 8 ? 8 : n);
+    return e ? std::atoi(e) : 0;
   }();
-  return v;
+  const int n = v > 0 ? v : dflt;
+  return n < 1 ? 1 : (n > 8 ? 8 : n);
 }
 
 template <int NP>
@@ -1174,11 +1260,12 @@ cudaError_t launch_colp(const KParams& p0, cudaStream_t s) {
   std::memset(&map4, 0, sizeof(map4));
   if (!make_o1_plane_map(&map, p0) || !make_o1_plane_map(&map4, p0, kRPS)) return cudaErrorNotSupported;
   auto kern = k_col_o1p<NP>;
+  constexpr int threads = 32 * (NP + 1 + colp_folders<NP>());
   // dynamic shared memory padded so that at most o1p_ctas_per_sm() CTAs fit on an SM
   int dev = 0, smem_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-  const int ctas = o1p_ctas_per_sm();
+  const int ctas = o1p_ctas_per_sm(colp_ctas<NP>());
   // ring depth: every stage the CTA's share of the SM's shared memory holds (a deep ring is what
   // hides the TMA latency: each step's compute is short), NP <= stages <= kPDMax
   const size_t cap = std::min<size_t>((size_t)(smem_sm > 0 ? smem_sm : 233472) / ctas - 1024, 227 * 1024);
@@ -1194,7 +1281,7 @@ cudaError_t launch_colp(const KParams& p0, cudaStream_t s) {
   });
   if (e != cudaSuccess) return e;
   int blocks = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, 32 * (NP + 1), smem) != cudaSuccess || blocks < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, threads, smem) != cudaSuccess || blocks < 1)
     blocks = 1;
   KParams p = p0;
   p.o1_stages = nst;
@@ -1222,7 +1309,7 @@ cudaError_t launch_colp(const KParams& p0, cudaStream_t s) {
     p.o1_nseg_y = (p.out_rows + p.o1_seg_y - 1) / p.o1_seg_y;
   }
   const long long nt = ncb * p.o1_nseg_y * p.B;
-  return launch_k(kern, dim3((unsigned)nt), dim3(32 * (NP + 1)), smem, s, p.ev[1] == nullptr, map, map4, p);
+  return launch_k(kern, dim3((unsigned)nt), dim3(threads), smem, s, p.ev[1] == nullptr, map, map4, p);
 }
 
 template <int G, int LO, int HI>

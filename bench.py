@@ -324,6 +324,11 @@ def _cpu_crop(cfg, blk, sigma_s):
     return np.ascontiguousarray(rows[:, xa:xb]), (r0 - ya, c0 - xa, br, bw, ya == 0 and yb == cfg.H, xa, xb)
 
 
+def _cpu_worker_warm(_):
+    import oracle  # noqa: F401
+    return os.getpid()
+
+
 def _cpu_block_work(args):
     """Worker: oracle.gc_filter_rows on one crop (the oracle as it stands, numpy fp64)."""
     crop, (ry, cx, br, bw, _, _, _), sigma_s, sigma_r, N = args
@@ -346,7 +351,11 @@ class CpuOracle:
         self.cores = cores or len(os.sched_getaffinity(0))
         self.blocks = _cpu_blocks(cfg, self.cores)
         self.crops = [_cpu_crop(cfg, b, sigma_s) for b in self.blocks]
-        self.pool = mp.get_context("fork").Pool(self.cores) if self.cores > 1 else None
+        # forkserver, not fork: the bench process holds a CUDA context and helper threads (NVML
+        # sampler, CUDA runtime) whose locks a forked child could inherit mid-operation
+        self.pool = mp.get_context("forkserver").Pool(self.cores) if self.cores > 1 else None
+        if self.pool:                              # workers import the oracle before any timing
+            self.pool.map(_cpu_worker_warm, range(self.cores), chunksize=1)
 
     def close(self):
         if self.pool:
@@ -358,7 +367,7 @@ class CpuOracle:
         n = cores or self.cores
         work = [(c, m, self.sigma_s, self.sigma_r, self.N) for c, m in self.crops[:n]]
         t0 = time.perf_counter()
-        if n == 1 or self.pool is None:
+        if self.pool is None:
             res = [_cpu_block_work(w) for w in work]
         else:
             res = self.pool.map(_cpu_block_work, work, chunksize=1)

@@ -353,6 +353,12 @@ __device__ __forceinline__ void row_o1_task(const KParams& p, RowO1Smem& sm, int
   // leaving stream's first chunk: staged here unless x = xs itself starts a chunk (then the first
   // step stages it; staging it twice would read the prefetch of the chunk after it)
   if ((xs - R) & (kO1CH - 1)) o1_stage_row<0, PM>(p, sm.fout, sm.raw[1], rowp, (xs - R) & ~(kO1CH - 1), lane, vec, p0);
+  // row_o1_step stages with wait_group 1, which assumes the newest cp.async group is the OTHER
+  // stream's prefetch.  After the staging above the only group in flight is the leaving stream's
+  // own prefetch, and for R mod 16 in 1..7 the leaving stream stages again before the entering
+  // stream does: wait_group 1 would let it read raw[1] before that prefetch landed (stale samples,
+  // a timing-dependent error in the window sum).  An empty group restores the invariant.
+  asm volatile("cp.async.commit_group;" ::: "memory");
   // O(1) plane layout [B][rows][NP][Wd]: the NP pairs of one image row are adjacent rows of
   // a 2-D [B*rows*NP][Wd] tensor, so the column pass fetches a row's pairs with one TMA box
   const long long rstride = (long long)p.NP * p.Wd;         // float2 between image rows

@@ -78,6 +78,7 @@ def test_gaussian_vs_oracle(gc, op, sigma_s, H, W):
     ("c3", 40.0, 130, 170),
     ("c3", 40.0, 700, 650),
     ("c4", 4.0, 129, 1024),
+    ("c5", 6.0, 400, 333),     # W = 18: leaving stream pre-staged, stages first (gc_o1.cu row_o1_task)
     ("c5", 16.0, 300, 290),
     ("c5", 16.0, 1030, 1100),
 ])

@@ -1020,18 +1020,32 @@ __global__ void __launch_bounds__(32 * (NP + 1 + colp_folders<NP>()), colp_ctas<
       }
     } else {
       const int fi = warp - NP - 1;                 // the row of every block this warp folds
+      // f of the row folded kFPD blocks later, loaded now: the fold warps set the pace of the
+      // pass (the consumers wait on tile_free), and one block did not cover the DRAM latency of
+      // f (ncu r02fin3: the fold's first use of f was 9 % of the stall samples; r02bo: c5 column
+      // pass 6.16-6.32 -> 5.88-5.97 ms at kFPD = 3)
+#ifndef GC_COLP_FOLD_PREFETCH
+#define GC_COLP_FOLD_PREFETCH 3
+#endif
+      constexpr int kFPD = GC_COLP_FOLD_PREFETCH;
+      const float* const frun = row_run_ptr(p, b, p.out_row0 + ys, ye - ys);   // null if the strip spans segments
       auto frow = [&](int blk) -> float {           // f at row fi of block blk (0 past the strip)
         const int r = ys + blk * kRPS + fi;
         if (blk >= nblk || r >= ye) return 0.f;
-        GC_CHK(p, row_ptr(p, b, p.out_row0 + r) + xc, 4);
-        return __ldg(row_ptr(p, b, p.out_row0 + r) + xc);
+        const float* a = frun ? frun + (long long)(r - ys) * p.Wd + xc : row_ptr(p, b, p.out_row0 + r) + xc;
+        GC_CHK(p, a, 4);
+        return __ldg(a);
       };
-      float fo_next = frow(0);
+      float fq[kFPD];
+#pragma unroll
+      for (int k = 0; k < kFPD; k++) fq[k] = frow(k);
 #pragma unroll 1
       for (int blk = 0; blk < nblk; blk++) {
         const int r = ys + blk * kRPS + fi;
-        const float fo = fo_next;
-        fo_next = frow(blk + 1);                    // one block ahead: this warp has the time
+        const float fo = fq[0];
+#pragma unroll
+        for (int k = 0; k + 1 < kFPD; k++) fq[k] = fq[k + 1];
+        fq[kFPD - 1] = frow(blk + kFPD);
         // (wait even when row fi lies past the strip's end: an arrival on tile_free before block
         // blk is in could complete the buffer's previous phase while another fold warp still
         // reads it — fold warps do not filter, so nothing else keeps them within a phase)
